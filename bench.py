@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark: batched HQC.PKE.Decrypt decryptions/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--level 3] [--batch 65536] [--impl ours|reference]
+
+A step = one pass of the whole hot path (stages 1-3, the fused kernel) over the rank's resident batch.
+N > 1 runs under torchrun, one process per GPU; each rank owns ciphertexts [rank*B, (rank+1)*B) of
+the same seeded workload (weak scaling, no collective in the timed region); time = max over ranks
+of the CUDA-event time; rank 0 prints ONE JSON line. See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HQC-1/3/5 PKE decryptions/sec per B200 and 8xB200; fraction of roofline"
+CONFIG_SEED = {1: 0xC0F1_0001, 3: 0xC0F1_0002, 5: 0xC0F1_0003}
+WORKLOAD = {1: "configs[0]-shape HQC-1 PKE decrypt", 3: "configs[1] HQC-3 PKE decrypt, batch 65536/GPU",
+            5: "configs[2] HQC-5 PKE decrypt"}
+
+
+def algorithmic_ops(p) -> dict:
+    """Integer ops per ciphertext the method itself must do."""
+    pairs = p.w * p.n12 // 32
+    s1 = pairs * 3 // 2
+    s2 = p.n1 * (128 + 896 + 128)
+    d = p.delta
+    s3 = 3 * (2 * d * p.n1 + 4 * d * (d + 1) + p.n1 * (d + 1) + 2 * d * p.k)
+    hbm = (p.n + 7) // 8 + p.n12 // 8 + 2 * p.w + p.k
+    return dict(stage1=s1, stage2=s2, stage3=s3, total=s1 + s2 + s3, pairs=pairs, hbm_bytes=hbm,
+                abi_bytes=8 * p.u_stride + 8 * p.v_words + 4 * p.y_stride + p.k)
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(level: int, i0: int, B: int, p, nthreads=None):
+    """Seeded synthetic ciphertexts. v0: uniformly random u and v with the key's y
+    (config 4's fourth-quarter construction): the decrypt path is constant-flow, so its throughput
+    does not depend on whether the ciphertext decodes."""
+    from paper_2512_12904_b200 import gen
+
+    seed = CONFIG_SEED[level]
+    key = gen.key_of(i0, B)
+    k0, nk = int(key[0]), int(key[-1] - key[0] + 1)
+    y_keys = gen.support(seed, gen.TAG_Y, k0, nk, p.n, p.w, p.y_stride, nthreads)
+    y = np.ascontiguousarray(y_keys[key - k0])
+    u = gen.dense(seed, gen.TAG_U_RAND, i0, B, p.n, p.u_stride, nthreads)
+    v = gen.dense(seed, gen.TAG_V_RAND, i0, B, p.n12, p.v_words, nthreads)
+    return u, v, y
+
+
+def cpu_baseline(level: int, u, v, y, got: np.ndarray | None, budget_s: float = 12.0) -> dict:
+    """The oracle, as it stands, on this host's cores over a bounded sample of the same inputs."""
+    import oracle
+
+    op = oracle.params(level)
+    cores = os.cpu_count() or 1
+    done, t_total, n = 0, 0.0, max(cores, 64)
+    mism = 0
+    while t_total < budget_s and done < u.shape[0]:
+        n = min(n, u.shape[0] - done)
+        sl = slice(done, done + n)
+        t0 = time.perf_counter()
+        m = oracle.decrypt_batch(op, u[sl], v[sl], y[sl], nthreads=cores)
+        t_total += time.perf_counter() - t0
+        if got is not None:
+            mism += int((m != got[sl]).any(axis=1).sum())
+        done += n
+        n *= 2
+    return {"value": done / t_total, "unit": "decryptions/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {done} ciphertexts of this rank's batch, oracle decrypt on {cores} threads "
+                      f"({t_total:.1f} s)", "parity_mismatches_vs_gpu": mism}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_2512_12904_b200 import gen  # noqa: F401  (input generator only)
+    import oracle
+
+    op = oracle.params(args.level)
+
+    class P:  # the generator needs only sizes
+        n, w, n12 = op.n, op.w, op.n12
+        u_stride = op.words + (op.words & 1)
+        v_words = op.vwords
+        y_stride = (op.w + 3) // 4 * 4
+
+    cores = os.cpu_count() or 1
+    per_step = max(cores * 8, 64)
+    u, v, y = make_inputs(args.level, 0, per_step, P)
+    for _ in range(args.warmup):
+        oracle.decrypt_batch(op, u[:cores], v[:cores], y[:cores], nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.decrypt_batch(op, u, v, y, nthreads=cores)
+    dt = time.perf_counter() - t0
+    val = per_step * args.steps / dt
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "decryptions/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32 (GF(2), GF(2^8))",
+           "data": "synthetic", "config": {"workload": WORKLOAD[args.level] + " (bounded CPU sample)",
+                                           "level": args.level, "batch_per_step": per_step},
+           "cpu_baseline": {"value": val, "unit": "decryptions/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{per_step} ciphertexts per step"},
+           "e2e": {"value": val, "unit": "decryptions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--level", type=int, default=3, choices=[1, 3, 5])
+    ap.add_argument("--batch", type=int, default=65536, help="ciphertexts per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_12904_b200 import hqc
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p = hqc.params(args.level)
+    B = args.batch
+    i0 = rank * B
+    u, v, y = make_inputs(args.level, i0, B, p)
+    du = torch.from_numpy(u.view(np.uint8)).to(dev)
+    dv = torch.from_numpy(v.view(np.uint8)).to(dev)
+    dy = torch.from_numpy(y.view(np.uint8)).to(dev)
+    dm = torch.empty(B * p.k, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        hqc.hqc_decrypt_batch(args.level, du, dv, dy, dm)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            hqc.hqc_decrypt_batch(args.level, du, dv, dy, dm)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- e2e: host (pinned) buffers through the same C-ABI call, copies inside the timed region
+    hu, hv, hy = (torch.from_numpy(a.view(np.uint8)).pin_memory() for a in (u, v, y))
+    hm = torch.empty(B * p.k, dtype=torch.uint8).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        du.copy_(hu, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        dy.copy_(hy, non_blocking=True)
+        hqc.hqc_decrypt_batch(args.level, du, dv, dy, dm)
+        hm.copy_(dm, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ems], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": world * B * args.e2e_steps / (ems / 1e3), "unit": "decryptions/s",
+           "h2d_bytes_per_step": int(u.nbytes + v.nbytes + y.nbytes), "d2h_bytes_per_step": int(B * p.k)}
+
+    got = dm.cpu().numpy().reshape(B, p.k)
+    ops = algorithmic_ops(p)
+    peaks = measured_peaks()
+    c = clk.summary()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    kernel_s = ms / 1e3 / args.steps
+    achieved_tops = ops["total"] * B / kernel_s / 1e12
+    peak_tops = 64 * sms * sm_max * 1e6 / 1e12  # ALU pipe: 64 lanes/clk/SM
+    roof = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Tintop/s",
+            "frac": achieved_tops / peak_tops, "traffic": None,
+            "peak_source": f"64 ALU lanes/clk/SM x {sms} SMs x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "ops_per_decryption": ops["total"],
+            "frac_at_measured_clock": (achieved_tops / (64 * sms * c["sm_mhz"] * 1e6 / 1e12)) if c["sm_mhz"] else None,
+            "hbm_gbs": ops["abi_bytes"] * B / kernel_s / 1e9,
+            "hbm_frac": ops["abi_bytes"] * B / kernel_s / 1e9 / float(peaks.get("hbm_gbs", 6538.6)),
+            "roofline_decryptions_per_s": peak_tops * 1e12 / ops["total"]}
+    gw = hqc.hqc_decrypt_launch_shape(args.level, B)
+    out = {"metric": METRIC, "value": value, "unit": "decryptions/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u8/u32 (GF(2), GF(2^8))",
+           "data": "synthetic: uniformly random u,v + seeded key supports (constant-flow path)",
+           "config": {"workload": WORKLOAD[args.level], "level": args.level, "batch_per_gpu": B,
+                      "global_batch": world * B, "parallelism": f"dp{world}",
+                      "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB > 126 MB L2, no flush needed",
+                      "launch": {"grid": gw[0], "warps_per_cta": gw[1]}},
+           "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
+           "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"]}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.level, u, v, y, got)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

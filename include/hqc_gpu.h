@@ -1,0 +1,126 @@
+/*
+ * hqc_gpu.h — C ABI of libhqcgpu.so: batched HQC.PKE.Decrypt on NVIDIA B200 (sm_100a).
+ *
+ * What it computes (PAPER.md = arxiv 2512.12904 "OptHQC"; P:n = line n; R#k = DESIGN.md §3 reading k):
+ *   HQC.PKE.Decrypt (Alg. 2): m' = C.Decode(v - u*y) over many independent ciphertexts,
+ *   in three stages:
+ *     (1) the sparse x dense cyclic product of Eq. 1 (§III.B) in GF(2)[X]/(X^n - 1),
+ *         XORed into v and truncated to n1*n2 bits (R#1-R#3);
+ *     (2) duplicated RM(1,7) decoding of each n2-bit block (Table I; R#9-R#12);
+ *     (3) shortened RS decoding over GF(2^8) (R#4-R#7): syndromes, Berlekamp–Massey,
+ *         Chien root search over the n1 positions, Forney error values, message-first output.
+ *   The results are bit-identical to the CPU oracle in oracle/ (tests/test_gpu_*.py).
+ *
+ * Conventions for every entry point
+ *   - All functions are host functions, reentrant, with no global mutable state.
+ *   - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless the name says
+ *     _host; they are allocated and owned by the caller and must be 16-byte aligned. The library
+ *     allocates no device memory. Outputs must not alias inputs.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Every call only
+ *     enqueues work on it and returns; asynchronous faults surface at the caller's next sync.
+ *   - batch == 0 returns HQC_OK and launches nothing. Argument checks run on the host before any
+ *     launch: unknown level (HQC_ERR_LEVEL), NULL pointer with batch > 0 (HQC_ERR_NULL), pointer not
+ *     16-byte aligned (HQC_ERR_ALIGN), batch > HQC_MAX_BATCH (HQC_ERR_SIZE). A failed launch returns
+ *     HQC_ERR_CUDA. RS decoding failure is a RESULT (uncorrected bytes), never an error.
+ *   - Bit order: bit t of a ring element is bit t%64 of uint64 word t/64 (little endian).
+ *   - Unchecked preconditions (checking costs a pass): y_support[b][0..w) are distinct and < n
+ *     (S:263); use hqc_validate_support in debug builds. A support entry >= n is treated as 0 (no
+ *     fault, unspecified output). Bits >= n of u and the padding words/entries of every row are
+ *     ignored.
+ */
+#ifndef HQC_GPU_H
+#define HQC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HQC_OK = 0,
+  HQC_ERR_LEVEL = -1,
+  HQC_ERR_NULL = -2,
+  HQC_ERR_ALIGN = -3,
+  HQC_ERR_SIZE = -4,
+  HQC_ERR_CUDA = -5
+} hqc_status;
+
+#define HQC_MAX_BATCH ((size_t)1 << 31)
+
+/* Table I plus the derived row layout of this library. Filled by hqc_get_params;
+   treat as read-only. */
+typedef struct {
+  int32_t level;     /* 1, 3, 5 */
+  uint32_t n;        /* ring length N: 17669 / 35851 / 57637 */
+  uint32_t n1;       /* RS length: 46 / 56 / 90 */
+  uint32_t n2;       /* duplicated RM length: 384 / 640 / 640 */
+  uint32_t mult;     /* n2 / 128: 3 / 5 / 5 */
+  uint32_t k;        /* message bytes: 16 / 24 / 32 */
+  uint32_t delta;    /* RS correction capacity (d-1)/2: 15 / 16 / 29 */
+  uint32_t w;        /* omega, weight of y: 66 / 100 / 131 */
+  uint32_t wr;       /* omega_r = omega_e: 75 / 114 / 149 */
+  uint32_t n12;      /* n1*n2: 17664 / 35840 / 57600 */
+  uint32_t u_words;  /* ceil(n/64): 277 / 561 / 901 */
+  uint32_t u_stride; /* uint64 per u row = u_words rounded up to even (16-byte rows) */
+  uint32_t v_words;  /* uint64 per v / r row = n12/64: 276 / 560 / 900 */
+  uint32_t y_stride; /* uint32 per support row = w rounded up to a multiple of 4 */
+  uint32_t e_stride; /* uint32 per r1/r2/e support row = wr rounded up to a multiple of 4 */
+} hqc_params;
+
+/* Fills *out for level 1, 3 or 5. Returns HQC_OK or HQC_ERR_LEVEL / HQC_ERR_NULL. */
+int hqc_get_params(int level, hqc_params *out);
+
+/* Static string for a status code (never NULL). */
+const char *hqc_status_str(int status);
+
+/* ---------------------------------------------------------------------------------------------
+ * Fused decrypt (Alg. 2):  m_out[b] = C.Decode(v[b] XOR trunc_{n12}(u[b] * y[b]))
+ *   u         [batch][u_stride] uint64   ciphertext part u (bits >= n ignored)
+ *   v         [batch][v_words]  uint64   ciphertext part v (n1*n2 bits)
+ *   y_support [batch][y_stride] uint32   the secret y's support, first w entries used (R#1)
+ *   m_out     [batch][k]        uint8    decrypted messages (RS failure -> uncorrected bytes)
+ * One kernel: stage 1 warp-per-ciphertext in shared memory, stage 2 lane-per-RM-block, stage 3
+ * lane-per-ciphertext; no intermediate leaves the SM.
+ * ------------------------------------------------------------------------------------------- */
+int hqc_decrypt_batch(const hqc_params *p, const uint64_t *u, const uint64_t *v,
+                      const uint32_t *y_support, uint8_t *m_out, size_t batch, void *stream);
+
+/* Stage 1 alone (Eq. 1; truncation R#3):
+ *   r_out[b] = v[b] XOR trunc_{n12}(u[b] * y[b]), [batch][v_words] uint64.
+ *   v may be NULL: r_out is then the truncated product alone (the standalone sparse x dense
+ *   product of BASELINE configs[4]). */
+int hqc_sparse_dense_mul_batch(const hqc_params *p, const uint64_t *u, const uint32_t *y_support,
+                               const uint64_t *v, uint64_t *r_out, size_t batch, void *stream);
+
+/* Stage 2 alone: sym_out[b][j] = RM-decode(bits [j*n2, (j+1)*n2) of r[b]), j < n1 (R#9-R#11).
+ *   r [batch][v_words] uint64 -> sym_out [batch][n1] uint8. */
+int hqc_rm_decode_batch(const hqc_params *p, const uint64_t *r, uint8_t *sym_out, size_t batch,
+                        void *stream);
+
+/* Stage 3 alone: m_out[b] = RS-decode(sym[b]) (bounded-distance decoding, R#7).
+ *   sym [batch][n1] uint8 -> m_out [batch][k] uint8; ok_out [batch] (nullable) = 1 if a codeword
+ *   within distance delta was found (and corrected), else 0 (m_out = sym[b][0..k)). */
+int hqc_rs_decode_batch(const hqc_params *p, const uint8_t *sym, uint8_t *m_out, size_t batch,
+                        void *stream);
+int hqc_rs_decode_batch_ex(const hqc_params *p, const uint8_t *sym, uint8_t *m_out,
+                           uint8_t *ok_out, size_t batch, void *stream);
+
+/* Helpers for tests and the bench.
+ * hqc_count_mismatch: *d_count += #{b : m_out[b] != m_ref[b]} (d_count: one device uint64, the
+ *   caller zeroes it). hqc_validate_support: *d_bad += #{rows with an entry >= n or a repeated
+ *   entry among the first w}. */
+int hqc_count_mismatch(const hqc_params *p, const uint8_t *m_out, const uint8_t *m_ref,
+                       size_t batch, unsigned long long *d_count, void *stream);
+int hqc_validate_support(const hqc_params *p, const uint32_t *y_support, size_t batch,
+                         unsigned long long *d_bad, void *stream);
+
+/* Number of persistent CTAs / warps the fused kernel launches for `batch` on the current device
+ * (introspection for the bench's launch accounting). Returns HQC_OK. */
+int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HQC_GPU_H */

@@ -18,11 +18,7 @@ static void put_bit(uint64_t *v, uint32_t t, int b) {
   uint64_t m = 1ull << (t % 64);
   if (b) v[t / 64] |= m; else v[t / 64] &= ~m;
 }
-static int parity8(uint32_t x) {
-  int p = 0;
-  for (int i = 0; i < 8; i++) p ^= (x >> i) & 1;
-  return p;
-}
+static int parity8(uint32_t x) { return __builtin_parity(x & 0xFFu); } /* XOR of the 8 low bits */
 
 void orc_rm_encode(uint8_t b, uint32_t mult, uint64_t *vec, uint32_t off) {
   for (uint32_t c = 0; c < mult; c++)

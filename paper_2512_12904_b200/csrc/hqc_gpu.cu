@@ -1,0 +1,411 @@
+// libhqcgpu.so — kernels and C ABI (include/hqc_gpu.h). DESIGN.md §6 describes each kernel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/hqc_gpu.h"
+#include "gf256.cuh"
+#include "levels.cuh"
+#include "stage1.cuh"
+#include "stage2.cuh"
+#include "stage3.cuh"
+
+namespace hqc {
+
+// ------------------------------------------------------------------------------------------------
+// Shared-memory carve-up of the fused / stage-1 kernels (per warp), 16-byte aligned pieces.
+template <class P> struct WarpSmem {
+  static constexpr uint32_t E_BYTES = round_up(
+      (P::E_WORDS * 4 > S3Scratch<P>::BYTES ? P::E_WORDS * 4 : S3Scratch<P>::BYTES), 16);
+  static constexpr uint32_t D_BYTES = round_up(P::WPAD * 4, 16);
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 32, 16);
+  static constexpr uint32_t BYTES = E_BYTES + D_BYTES + SYM_BYTES;
+};
+constexpr uint32_t GF_BYTES = round_up(sizeof(GfTables), 16);
+
+// ------------------------------------------------------------------------------------------------
+// K1: stage 1 alone. One warp per ciphertext (grid-stride over warps).
+template <class P>
+__global__ void __launch_bounds__(128) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
+                                                const uint64_t *__restrict__ v, uint64_t *__restrict__ r_out,
+                                                size_t batch) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t *ws = smem + (size_t)wib * (WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES);
+  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + WarpSmem<P>::E_BYTES);
+  const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib; ct < batch; ct += nwarps) {
+    s1_run<P>(u + ct * P::U_STRIDE, y + ct * P::Y_STRIDE, v ? v + ct * P::V_WORDS : nullptr, E, dsm, lane);
+    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
+    const uint4 *src = reinterpret_cast<const uint4 *>(E);
+    for (uint32_t c = lane; c < P::NW / 4; c += 32) dst[c] = src[c];
+    __syncwarp();
+  }
+}
+
+// K2: stage 2 alone. One thread per RM block.
+template <class P>
+__global__ void __launch_bounds__(128) k_stage2(const uint64_t *__restrict__ r, uint8_t *__restrict__ sym,
+                                                size_t nblocks) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblocks) return;
+  const size_t ct = t / P::N1, j = t % P::N1;
+  const uint4 *src = reinterpret_cast<const uint4 *>(r + ct * P::V_WORDS) + j * (P::N2 / 128);
+  uint32_t X[P::MULT * 4];
+#pragma unroll
+  for (int c = 0; c < (int)P::MULT; c++) {
+    const uint4 x = __ldg(src + c);
+    X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+  }
+  sym[t] = (uint8_t)rm_decode_block<P::MULT>(X);
+}
+
+// K3: stage 3 alone. One thread per ciphertext; a warp stages its 32 rows of symbols into shared
+// memory as [j][lane] so every later access is conflict-free.
+template <class P>
+__global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym, uint8_t *__restrict__ m_out,
+                                                uint8_t *__restrict__ ok_out, size_t batch) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + (size_t)wib * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
+  uint16_t *scr = reinterpret_cast<uint16_t *>(ws);
+  uint8_t *sb = ws + S3Scratch<P>::BYTES;
+  const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t base = ((size_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; base < batch; base += nwarps * 32) {
+    const size_t rows = batch - base < 32 ? batch - base : 32;
+    for (uint32_t e = lane; e < 32 * P::N1; e += 32) {  // e = row*N1 + j (coalesced read)
+      const uint32_t row = e / P::N1, j = e % P::N1;
+      sb[j * 32 + row] = row < rows ? sym[(base + row) * P::N1 + j] : 0;
+    }
+    __syncwarp();
+    const bool act = (size_t)lane < rows;
+    auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
+    const uint32_t ok = rs_decode_lane<P>(sym_at, gf, scr, lane, act ? m_out + (base + lane) * P::K : nullptr);
+    if (act && ok_out) ok_out[base + lane] = (uint8_t)ok;
+    __syncwarp();
+  }
+}
+
+// K4: fused decrypt. Persistent warps; warp g owns ciphertexts [g*per, (g+1)*per) and walks them in
+// chunks of 32: stage 1 (whole warp) and stage 2 (lane per RM block) per ciphertext, symbols parked
+// in shared memory as [j][slot]; then stage 3 with one lane per ciphertext of the chunk.
+template <class P>
+__global__ void __launch_bounds__(128) k_decrypt(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
+                                                 const uint32_t *__restrict__ y, uint8_t *__restrict__ m_out,
+                                                 size_t batch, size_t per) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + (size_t)wib * WarpSmem<P>::BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + WarpSmem<P>::E_BYTES);
+  uint8_t *sb = ws + WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES;
+  const size_t g = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const size_t lo = g * per;
+  const size_t hi = lo + per < batch ? lo + per : batch;
+  for (size_t base = lo; base < hi; base += 32) {
+    const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
+    for (uint32_t s = 0; s < rows; s++) {
+      const size_t ct = base + s;
+      s1_run<P>(u + ct * P::U_STRIDE, y + ct * P::Y_STRIDE, v + ct * P::V_WORDS, E, dsm, lane);
+      for (uint32_t j = lane; j < P::N1; j += 32) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(E) + j * (P::N2 / 128);
+        uint32_t X[P::MULT * 4];
+#pragma unroll
+        for (int c = 0; c < (int)P::MULT; c++) {
+          const uint4 x = src[c];
+          X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+        }
+        sb[j * 32 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+      }
+      __syncwarp();
+    }
+    for (uint32_t s = rows; s < 32; s++)
+      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * 32 + s] = 0;
+    __syncwarp();
+    const bool act = (uint32_t)lane < rows;
+    auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
+    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(E), lane, act ? m_out + (base + lane) * P::K : nullptr);
+    __syncwarp();
+  }
+}
+
+__global__ void k_count_mismatch(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, uint32_t k,
+                                 size_t batch, unsigned long long *count) {
+  unsigned long long local = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t diff = 0;
+    for (uint32_t j = 0; j < k; j++) diff |= a[i * k + j] ^ b[i * k + j];
+    local += diff != 0;
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+__global__ void k_validate_support(const uint32_t *__restrict__ y, uint32_t n, uint32_t w, uint32_t stride,
+                                   size_t batch, unsigned long long *bad) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t *row = y + i * stride;
+    bool b = false;
+    for (uint32_t j = 0; j < w; j++) {
+      const uint32_t x = row[j];
+      b |= x >= n;
+      for (uint32_t t = 0; t < j; t++) b |= row[t] == x;
+    }
+    if (b) atomicAdd(bad, 1ull);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+struct DevInfo {
+  int sms = 0;
+  int cap_decrypt[6] = {0};  // resident CTAs/SM of k_decrypt per level
+  int cap_stage1[6] = {0};
+  bool ready[6] = {false};
+};
+
+static std::mutex g_mu;
+static DevInfo g_dev[16];
+
+constexpr int WARPS_PER_CTA = 1;  // fused / stage-1 kernels: one warp per CTA (fine-grained SM balance)
+
+template <class P> static uint32_t decrypt_smem() { return GF_BYTES + WARPS_PER_CTA * WarpSmem<P>::BYTES; }
+template <class P> static uint32_t stage1_smem() {
+  return WARPS_PER_CTA * (WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES);
+}
+template <class P> static uint32_t stage3_smem(int warps) {
+  return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
+}
+
+template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (di.ready[P::level]) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_decrypt<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_stage1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_stage3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage3_smem<P>(4))) != cudaSuccess) return e;
+  int c = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt<P>, 32 * WARPS_PER_CTA, decrypt_smem<P>())) != cudaSuccess) return e;
+  di.cap_decrypt[P::level] = c > 0 ? c : 1;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
+  di.cap_stage1[P::level] = c > 0 ? c : 1;
+  di.ready[P::level] = true;
+  return cudaSuccess;
+}
+
+static int cur_device(DevInfo **out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return -1;
+  *out = &g_dev[dev];
+  return dev;
+}
+
+template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
+  const size_t cap = (size_t)di.sms * di.cap_decrypt[P::level] * WARPS_PER_CTA;
+  size_t warps = (batch + 31) / 32;
+  if (warps > cap) warps = cap;
+  if (warps == 0) warps = 1;
+  *per = (batch + warps - 1) / warps;
+  const size_t used = (batch + *per - 1) / *per;
+  *grid = (int)((used + WARPS_PER_CTA - 1) / WARPS_PER_CTA);
+}
+
+template <class P>
+static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *y, uint8_t *m, size_t batch,
+                          cudaStream_t st) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  int grid;
+  size_t per;
+  decrypt_shape<P>(*di, batch, &grid, &per);
+  k_decrypt<P><<<grid, 32 * WARPS_PER_CTA, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v, uint64_t *r, size_t batch,
+                         cudaStream_t st) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  const size_t cap = (size_t)di->sms * di->cap_stage1[P::level];
+  size_t grid = (batch + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  if (grid > cap) grid = cap;
+  k_stage1<P><<<(unsigned)grid, 32 * WARPS_PER_CTA, stage1_smem<P>(), st>>>(u, y, v, r, batch);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P> static int launch_stage2(const uint64_t *r, uint8_t *sym, size_t batch, cudaStream_t st) {
+  const size_t nb = batch * P::N1;
+  const size_t grid = (nb + 127) / 128;
+  k_stage2<P><<<(unsigned)grid, 128, 0, st>>>(r, sym, nb);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_stage3(const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t batch, cudaStream_t st) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  const int warps = 4;
+  size_t grid = (batch + 32 * warps - 1) / (32 * warps);
+  const size_t cap = (size_t)di->sms * 16;
+  if (grid > cap) grid = cap;
+  k_stage3<P><<<(unsigned)grid, 32 * warps, stage3_smem<P>(warps), st>>>(sym, m, ok, batch);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+}  // namespace hqc
+
+// ================================================================================================
+// C ABI
+using namespace hqc;
+
+template <int L> static void fill_params(hqc_params *o) {
+  using P = Lv<L>;
+  o->level = L;
+  o->n = P::N; o->n1 = P::N1; o->n2 = P::N2; o->mult = P::MULT; o->k = P::K; o->delta = P::DELTA;
+  o->w = P::W; o->wr = P::WR; o->n12 = P::N12; o->u_words = P::U_WORDS; o->u_stride = P::U_STRIDE;
+  o->v_words = P::V_WORDS; o->y_stride = P::Y_STRIDE; o->e_stride = P::E_STRIDE;
+}
+
+extern "C" int hqc_get_params(int level, hqc_params *out) {
+  if (!out) return HQC_ERR_NULL;
+  switch (level) {
+    case 1: fill_params<1>(out); return HQC_OK;
+    case 3: fill_params<3>(out); return HQC_OK;
+    case 5: fill_params<5>(out); return HQC_OK;
+    default: return HQC_ERR_LEVEL;
+  }
+}
+
+extern "C" const char *hqc_status_str(int s) {
+  switch (s) {
+    case HQC_OK: return "ok";
+    case HQC_ERR_LEVEL: return "unknown parameter level";
+    case HQC_ERR_NULL: return "null pointer";
+    case HQC_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case HQC_ERR_SIZE: return "batch too large";
+    case HQC_ERR_CUDA: return "CUDA launch error";
+    default: return "unknown status";
+  }
+}
+
+static int check_level(const hqc_params *p) {
+  if (!p) return HQC_ERR_NULL;
+  if (p->level != 1 && p->level != 3 && p->level != 5) return HQC_ERR_LEVEL;
+  return HQC_OK;
+}
+static bool misaligned(const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) != 0; }
+
+#define HQC_CHECK_PTR(q)                 \
+  do {                                   \
+    if (!(q)) return HQC_ERR_NULL;       \
+    if (misaligned(q)) return HQC_ERR_ALIGN; \
+  } while (0)
+
+#define HQC_DISPATCH(p, fn, ...)                                 \
+  switch ((p)->level) {                                          \
+    case 1: return fn<Lv<1>>(__VA_ARGS__);                       \
+    case 3: return fn<Lv<3>>(__VA_ARGS__);                       \
+    default: return fn<Lv<5>>(__VA_ARGS__);                      \
+  }
+
+extern "C" int hqc_decrypt_batch(const hqc_params *p, const uint64_t *u, const uint64_t *v,
+                                 const uint32_t *y, uint8_t *m, size_t batch, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(u); HQC_CHECK_PTR(v); HQC_CHECK_PTR(y); HQC_CHECK_PTR(m);
+  HQC_DISPATCH(p, launch_decrypt, u, v, y, m, batch, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_sparse_dense_mul_batch(const hqc_params *p, const uint64_t *u, const uint32_t *y,
+                                          const uint64_t *v, uint64_t *r, size_t batch, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(u); HQC_CHECK_PTR(y); HQC_CHECK_PTR(r);
+  if (v && misaligned(v)) return HQC_ERR_ALIGN;
+  HQC_DISPATCH(p, launch_stage1, u, y, v, r, batch, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_rm_decode_batch(const hqc_params *p, const uint64_t *r, uint8_t *sym, size_t batch,
+                                   void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(r); HQC_CHECK_PTR(sym);
+  HQC_DISPATCH(p, launch_stage2, r, sym, batch, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_rs_decode_batch_ex(const hqc_params *p, const uint8_t *sym, uint8_t *m, uint8_t *ok,
+                                      size_t batch, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(sym); HQC_CHECK_PTR(m);
+  if (ok && misaligned(ok)) return HQC_ERR_ALIGN;
+  HQC_DISPATCH(p, launch_stage3, sym, m, ok, batch, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_rs_decode_batch(const hqc_params *p, const uint8_t *sym, uint8_t *m, size_t batch,
+                                   void *stream) {
+  return hqc_rs_decode_batch_ex(p, sym, m, nullptr, batch, stream);
+}
+
+extern "C" int hqc_count_mismatch(const hqc_params *p, const uint8_t *a, const uint8_t *b, size_t batch,
+                                  unsigned long long *count, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (!a || !b || !count) return HQC_ERR_NULL;
+  size_t grid = (batch + 255) / 256;
+  if (grid > 4096) grid = 4096;
+  k_count_mismatch<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a, b, p->k, batch, count);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+extern "C" int hqc_validate_support(const hqc_params *p, const uint32_t *y, size_t batch,
+                                    unsigned long long *bad, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (!y || !bad) return HQC_ERR_NULL;
+  size_t grid = (batch + 255) / 256;
+  if (grid > 4096) grid = 4096;
+  k_validate_support<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(y, p->n, p->w, p->y_stride, batch, bad);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  size_t per;
+  decrypt_shape<P>(*di, batch, grid, &per);
+  *wpc = WARPS_PER_CTA;
+  return HQC_OK;
+}
+
+extern "C" int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *wpc) {
+  int s = check_level(p);
+  if (s) return s;
+  if (!grid || !wpc) return HQC_ERR_NULL;
+  HQC_DISPATCH(p, shape_impl, batch, grid, wpc);
+}

@@ -1,0 +1,46 @@
+// Compile-time parameter sets for the kernels (Table I; derived per DESIGN.md §3/§6).
+// Independent of oracle/ (tests cross-check hqc_get_params against the oracle's own table).
+#pragma once
+#include <cstdint>
+
+namespace hqc {
+
+template <int LEVEL> struct Table1;
+template <> struct Table1<1> { static constexpr uint32_t N = 17669, N1 = 46, N2 = 384, K = 16, D = 31, W = 66, WR = 75; };
+template <> struct Table1<3> { static constexpr uint32_t N = 35851, N1 = 56, N2 = 640, K = 24, D = 33, W = 100, WR = 114; };
+template <> struct Table1<5> { static constexpr uint32_t N = 57637, N1 = 90, N2 = 640, K = 32, D = 59, W = 131, WR = 149; };
+
+constexpr uint32_t round_up(uint32_t x, uint32_t m) { return (x + m - 1) / m * m; }
+constexpr uint32_t make_odd_up(uint32_t x) { return x | 1u; }
+
+template <int LEVEL> struct Lv : Table1<LEVEL> {
+  using T = Table1<LEVEL>;
+  static constexpr int level = LEVEL;
+  static constexpr uint32_t N = T::N, N1 = T::N1, N2 = T::N2, K = T::K, W = T::W, WR = T::WR;
+  static constexpr uint32_t MULT = N2 / 128;           // copies of RM(1,7)
+  static constexpr uint32_t DELTA = (T::D - 1) / 2;    // RS capacity (R#15)
+  static constexpr uint32_t TWO_DELTA = 2 * DELTA;     // = N1 - K syndromes / parity bytes
+  static constexpr uint32_t N12 = N1 * N2;             // truncation length (R#3)
+  static constexpr uint32_t NW = N12 / 32;             // 32-bit words of r (exact)
+  static constexpr uint32_t U_WORDS = (N + 63) / 64;
+  static constexpr uint32_t U_STRIDE = round_up(U_WORDS, 2);
+  static constexpr uint32_t V_WORDS = N12 / 64;
+  static constexpr uint32_t Y_STRIDE = round_up(W, 4);
+  static constexpr uint32_t E_STRIDE = round_up(WR, 4);
+  // stage 1: a warp owns one ciphertext; lane L owns R consecutive 32-bit output
+  // words [L*R, L*R+R). R is odd so that the 32 lanes' shared-memory reads E[o + L*R + k] fall in 32
+  // distinct banks for every (o, k).
+  static constexpr uint32_t R = make_odd_up((NW + 31) / 32);
+  static constexpr uint32_t Q0 = N / 32;               // word holding bit n-1
+  static constexpr uint32_t C = N % 32;                // bits of u in word Q0 (nonzero: n is prime)
+  // E[b] = u[b mod n] for b < 32*E_WORDS: the "doubled" u, so every rotation is a plain funnel shift
+  static constexpr uint32_t E_WORDS = round_up(Q0 + 32 * R + 2, 4);
+  static constexpr uint32_t WPAD = round_up(W, 4);     // d-values staged per warp
+  static_assert(C != 0, "n must not be a multiple of 32");
+  static_assert(N12 % 128 == 0, "r is processed in 16-byte chunks");
+  static_assert(N2 % 128 == 0 && (N2 / 32) % 4 == 0, "RM blocks are whole 16-byte chunks");
+  static_assert(N1 - K == TWO_DELTA, "shortened RS: n1 - k = 2 delta");
+  static_assert(K <= 32, "Forney root flags for message positions fit one 32-bit mask");
+};
+
+}  // namespace hqc

@@ -1,0 +1,110 @@
+// Stage 2 — duplicated RM(1,7) decoding of one n2-bit block by one thread (Table I P:113-117,
+// "byte-parallel Reed–Muller decoder" P:33; readings R#9-R#12 in DESIGN.md). DESIGN.md §6.2.
+//
+// The oracle defines F(a) = sum_p s_p (-1)^{a.p} with s_p = mult - 2*cnt_p (cnt_p = number of copies
+// with bit p set) and picks the smallest a with maximal |F(a)|, sign -> bit 7. Here:
+//   1. bit-sliced copy counting: cnt_p in 2 (mult 3) or 3 (mult 5) bit planes, 32 positions per op;
+//   2. cnt as exact fp16 in half2 registers: register i = 16q + l holds positions (32q+l, 32q+l+16);
+//      the value is built with the 1024-magic (0x6400 | cnt is the half 1024 + cnt);
+//   3. the 128-point fast Walsh–Hadamard transform: 6 butterfly stages across registers (HADD2 on
+//      the FMA pipe) and one in-register stage (HFMA2 with a (1,-1) multiplier). Every value is an
+//      integer of magnitude <= 640 < 2048, so fp16 arithmetic is exact;
+//   4. G(a) = F'(a) for a != 0, G(0) = F'(0) - 64*mult, where F' is the transform of cnt; then
+//      F = -2G, so argmax |F| = argmax |G| and F(a*) < 0 <=> G(a*) > 0;
+//   5. M = max |G| (HMNMX2 tree), then 128-bit masks of {|G| = M} and {G = M} in natural a order;
+//      a* = lowest set bit (smallest a, R#11), bit 7 = [G(a*) = M].
+#pragma once
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+namespace hqc {
+
+__device__ __forceinline__ __half2 u2h(uint32_t x) { return *reinterpret_cast<__half2 *>(&x); }
+
+// X[c*4 + q] = 32-bit word q of copy c of the block.
+template <int MULT>
+__device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4]) {
+  static_assert(MULT == 3 || MULT == 5, "duplicated RM(1,7) with 3 or 5 copies");
+  constexpr int NPL = (MULT == 3) ? 2 : 3;
+  uint32_t pl[NPL][4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t a = X[q], b = X[4 + q], c = X[8 + q];
+    const uint32_t s1 = a ^ b ^ c, c1 = (a & b) | (c & (a ^ b));  // full adder
+    if constexpr (MULT == 3) {
+      pl[0][q] = s1;
+      pl[1][q] = c1;
+    } else {
+      const uint32_t d = X[12 + q], e = X[16 + q];
+      const uint32_t s2 = s1 ^ d ^ e, c2 = (s1 & d) | (e & (s1 ^ d));  // full adder
+      pl[0][q] = s2;
+      pl[1][q] = c1 ^ c2;  // half adder of the two carries (weight 2)
+      pl[2][q] = c1 & c2;  // weight 4
+    }
+  }
+
+  __half2 h[64];
+  const __half2 k1024 = __float2half2_rn(1024.0f);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+#pragma unroll
+    for (int l = 0; l < 16; l++) {
+      uint32_t t = 0x64006400u | ((pl[0][q] >> l) & 0x00010001u) | (((pl[1][q] >> l) & 0x00010001u) << 1);
+      if constexpr (NPL == 3) t |= ((pl[2][q] >> l) & 0x00010001u) << 2;
+      h[16 * q + l] = __hsub2(u2h(t), k1024);
+    }
+  }
+
+  // FWHT over register-index bits 0..5 (position bits 0-3, 5, 6)
+#pragma unroll
+  for (int b = 0; b < 6; b++) {
+#pragma unroll
+    for (int i = 0; i < 64; i++) {
+      if (i & (1 << b)) continue;
+      const __half2 x = h[i], y = h[i | (1 << b)];
+      h[i] = __hadd2(x, y);
+      h[i | (1 << b)] = __hsub2(x, y);
+    }
+  }
+  // in-register stage over position bit 4: (lo, hi) -> (lo + hi, lo - hi)
+  const __half2 pm = __halves2half2(__float2half(1.0f), __float2half(-1.0f));
+#pragma unroll
+  for (int i = 0; i < 64; i++) h[i] = __hfma2(__high2half2(h[i]), pm, __low2half2(h[i]));
+  // a = 0 correction: G(0) = F'(0) - 64*mult
+  h[0] = __hsub2(h[0], __halves2half2(__float2half(64.0f * MULT), __float2half(0.0f)));
+
+  // M = max |G| (balanced tree for ILP)
+  __half2 m[32];
+#pragma unroll
+  for (int i = 0; i < 32; i++) m[i] = __hmax2(__habs2(h[i]), __habs2(h[i + 32]));
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1)
+#pragma unroll
+    for (int i = 0; i < s; i++) m[i] = __hmax2(m[i], m[i + s]);
+  const __half Mh = __hmax(__low2half(m[0]), __high2half(m[0]));
+  const __half2 M2 = __half2half2(Mh);
+
+  // masks in natural order: word q = i >> 4 holds a in [32q, 32q+32); bit (i&15) + 16*half
+  uint32_t absw[4] = {0u, 0u, 0u, 0u}, posw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 64; i++) {
+    const uint32_t bit = 0x00010001u << (i & 15);
+    absw[i >> 4] |= __heq2_mask(__habs2(h[i]), M2) & bit;
+    posw[i >> 4] |= __heq2_mask(h[i], M2) & bit;
+  }
+  // smallest a with |G(a)| = M (lowest set bit, lowest word first)
+  uint32_t a = 0, pw = 0;
+  bool found = false;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const bool take = !found && absw[q] != 0;
+    const uint32_t bitpos = __ffs(absw[q]) - 1;
+    a = take ? (32u * q + bitpos) : a;
+    pw = take ? (posw[q] >> bitpos) & 1u : pw;
+    found = found || take;
+  }
+  return a | (pw << 7);
+}
+
+}  // namespace hqc

@@ -1,0 +1,175 @@
+"""Thin Python binding of libhqcgpu.so (include/hqc_gpu.h): argument marshalling only.
+
+Every function takes torch CUDA tensors (any dtype view of the documented layout), passes their
+device pointers and the current torch stream to the C ABI, and raises on a nonzero status. All
+compute happens in the library's sm_100a kernels; there is no CPU or PyTorch fallback — a missing
+library raises ImportError-like RuntimeError at first use.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhqcgpu.so")
+
+
+class HqcError(RuntimeError):
+    pass
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32)] + [
+        (f, ctypes.c_uint32)
+        for f in ("n", "n1", "n2", "mult", "k", "delta", "w", "wr", "n12", "u_words", "u_stride", "v_words",
+                  "y_stride", "e_stride")
+    ]
+
+
+@dataclass(frozen=True)
+class Params:
+    level: int
+    n: int
+    n1: int
+    n2: int
+    mult: int
+    k: int
+    delta: int
+    w: int
+    wr: int
+    n12: int
+    u_words: int
+    u_stride: int
+    v_words: int
+    y_stride: int
+    e_stride: int
+
+
+_lib = None
+_cparams: dict[int, _Params] = {}
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HqcError(f"{LIB_PATH} is missing: build it with `python -m paper_2512_12904_b200.build` "
+                           "(or __graft_entry__.build()); there is no fallback path")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+        P = ctypes.POINTER(_Params)
+        sigs = {
+            "hqc_get_params": [i32, P],
+            "hqc_decrypt_batch": [P, vp, vp, vp, vp, sz, vp],
+            "hqc_sparse_dense_mul_batch": [P, vp, vp, vp, vp, sz, vp],
+            "hqc_rm_decode_batch": [P, vp, vp, sz, vp],
+            "hqc_rs_decode_batch": [P, vp, vp, sz, vp],
+            "hqc_rs_decode_batch_ex": [P, vp, vp, vp, sz, vp],
+            "hqc_count_mismatch": [P, vp, vp, sz, vp, vp],
+            "hqc_validate_support": [P, vp, sz, vp, vp],
+            "hqc_decrypt_launch_shape": [P, sz, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = i32
+        L.hqc_status_str.argtypes = [i32]
+        L.hqc_status_str.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _cp(level: int) -> _Params:
+    if level not in _cparams:
+        p = _Params()
+        _check(lib().hqc_get_params(level, ctypes.byref(p)))
+        _cparams[level] = p
+    return _cparams[level]
+
+
+def params(level: int) -> Params:
+    p = _cp(level)
+    return Params(*[getattr(p, f) for f, _ in _Params._fields_])
+
+
+def _check(status: int):
+    if status != 0:
+        raise HqcError(f"libhqcgpu: {lib().hqc_status_str(status).decode()} (status {status})")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise HqcError("libhqcgpu entry points take CUDA tensors (device pointers)")
+    if not t.is_contiguous():
+        raise HqcError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _rows(t, row_bytes: int, name: str) -> int:
+    nbytes = t.numel() * t.element_size()
+    if nbytes % row_bytes:
+        raise HqcError(f"{name}: {nbytes} bytes is not a whole number of {row_bytes}-byte rows")
+    return nbytes // row_bytes
+
+
+def hqc_decrypt_batch(level: int, u, v, y_support, m_out, stream=None) -> None:
+    """m_out[b] = C.Decode(v[b] ^ trunc(u[b] * y[b])) — the fused kernel."""
+    p = params(level)
+    B = _rows(u, 8 * p.u_stride, "u")
+    assert _rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B
+    assert _rows(m_out, p.k, "m_out") == B
+    _check(lib().hqc_decrypt_batch(ctypes.byref(_cp(level)), _ptr(u), _ptr(v), _ptr(y_support), _ptr(m_out), B,
+                                   _stream(stream)))
+
+
+def hqc_sparse_dense_mul_batch(level: int, u, y_support, v, r_out, stream=None) -> None:
+    p = params(level)
+    B = _rows(u, 8 * p.u_stride, "u")
+    assert _rows(r_out, 8 * p.v_words, "r_out") == B
+    _check(lib().hqc_sparse_dense_mul_batch(ctypes.byref(_cp(level)), _ptr(u), _ptr(y_support), _ptr(v),
+                                            _ptr(r_out), B, _stream(stream)))
+
+
+def hqc_rm_decode_batch(level: int, r, sym_out, stream=None) -> None:
+    p = params(level)
+    B = _rows(r, 8 * p.v_words, "r")
+    assert _rows(sym_out, p.n1, "sym_out") == B
+    _check(lib().hqc_rm_decode_batch(ctypes.byref(_cp(level)), _ptr(r), _ptr(sym_out), B, _stream(stream)))
+
+
+def hqc_rs_decode_batch(level: int, sym, m_out, ok_out=None, stream=None) -> None:
+    p = params(level)
+    B = _rows(sym, p.n1, "sym")
+    assert _rows(m_out, p.k, "m_out") == B
+    _check(lib().hqc_rs_decode_batch_ex(ctypes.byref(_cp(level)), _ptr(sym), _ptr(m_out), _ptr(ok_out), B,
+                                        _stream(stream)))
+
+
+def hqc_count_mismatch(level: int, m_out, m_ref, d_count, stream=None) -> None:
+    p = params(level)
+    B = _rows(m_out, p.k, "m_out")
+    _check(lib().hqc_count_mismatch(ctypes.byref(_cp(level)), _ptr(m_out), _ptr(m_ref), B, _ptr(d_count),
+                                    _stream(stream)))
+
+
+def hqc_validate_support(level: int, y_support, d_bad, stream=None) -> None:
+    p = params(level)
+    B = _rows(y_support, 4 * p.y_stride, "y")
+    _check(lib().hqc_validate_support(ctypes.byref(_cp(level)), _ptr(y_support), B, _ptr(d_bad),
+                                      _stream(stream)))
+
+
+def hqc_decrypt_launch_shape(level: int, batch: int) -> tuple[int, int]:
+    g, w = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().hqc_decrypt_launch_shape(ctypes.byref(_cp(level)), batch, ctypes.byref(g), ctypes.byref(w)))
+    return g.value, w.value

@@ -1,0 +1,76 @@
+"""CPU-side checks of the C ABI (no compute calls without a GPU): the library loads, exports every
+function include/hqc_gpu.h declares, hqc_get_params agrees with the oracle's independent Table I copy,
+and host-side argument validation returns the documented status codes before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+from paper_2512_12904_b200 import build as gpubuild
+from paper_2512_12904_b200 import hqc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    gpubuild.build()
+    return hqc.lib()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "hqc_gpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hqc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = declared_functions()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in include/hqc_gpu.h but not exported"
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_params_match_oracle(level, L):
+    g = hqc.params(level)
+    o = oracle.params(level)
+    for f in ("n", "n1", "n2", "mult", "k", "delta", "w", "wr", "n12"):
+        assert getattr(g, f) == getattr(o, f), f
+    assert g.u_words == o.words and g.v_words == o.vwords
+    assert g.u_stride % 2 == 0 and g.u_stride >= g.u_words
+    assert g.y_stride % 4 == 0 and g.y_stride >= g.w
+    assert g.e_stride % 4 == 0 and g.e_stride >= g.wr
+
+
+def test_host_validation(L):
+    P = hqc._Params
+    p = P()
+    assert L.hqc_get_params(1, ctypes.byref(p)) == 0
+    assert L.hqc_get_params(2, ctypes.byref(p)) == -1
+    assert L.hqc_get_params(1, None) == -2
+    L.hqc_get_params(1, ctypes.byref(p))
+    a16 = ctypes.c_void_p(0x1000)
+    a8 = ctypes.c_void_p(0x1008)
+    # batch 0 is a no-op even with NULL pointers
+    assert L.hqc_decrypt_batch(ctypes.byref(p), None, None, None, None, 0, None) == 0
+    assert L.hqc_decrypt_batch(ctypes.byref(p), None, a16, a16, a16, 4, None) == -2
+    assert L.hqc_decrypt_batch(ctypes.byref(p), a8, a16, a16, a16, 4, None) == -3
+    assert L.hqc_decrypt_batch(ctypes.byref(p), a16, a16, a16, a16, (1 << 31) + 1, None) == -4
+    bad = P()
+    ctypes.memmove(ctypes.byref(bad), ctypes.byref(p), ctypes.sizeof(P))
+    bad.level = 4
+    assert L.hqc_decrypt_batch(ctypes.byref(bad), a16, a16, a16, a16, 4, None) == -1
+    assert L.hqc_sparse_dense_mul_batch(ctypes.byref(p), a16, a16, a8, a16, 4, None) == -3
+    assert L.hqc_rm_decode_batch(ctypes.byref(p), a16, None, 4, None) == -2
+    assert L.hqc_rs_decode_batch(ctypes.byref(p), a16, a8, 4, None) == -3
+    assert L.hqc_status_str(-5) == b"CUDA launch error"
+
+
+def test_binding_refuses_cpu_tensors(L):
+    torch = pytest.importorskip("torch")
+    x = torch.zeros(64, dtype=torch.uint8)
+    with pytest.raises(hqc.HqcError):
+        hqc.hqc_rm_decode_batch(1, x, x)

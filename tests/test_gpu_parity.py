@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the ORACLE, element by element, on seeded
+inputs. Integer/bit work, so the bar is bit-exact. Marked gpu: needs a B200 and the built library.
+
+Sizes: small batches that span several chunks of 32 ciphertexts and a ragged tail, all three levels;
+adversarial (undecodable) inputs; stage-level garbage inputs; edge cases (batch 0/1, 33, supports at
+0 and n-1, all-zero ciphertext); and full BASELINE sizes in the bench's launch configuration with
+sampled oracle checks plus the whole-batch property decrypt(encrypt(m)) = m."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2512_12904_b200 import gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU only with -m gpu
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2512_12904_b200 import hqc  # noqa: E402
+from workloads import adversarial_batch, valid_batch  # noqa: E402
+
+DEV = torch.device("cuda:0")
+LEVELS = [1, 3, 5]
+
+
+def to_dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(DEV)
+
+
+def from_dev(t, dtype, cols):
+    return t.cpu().numpy().view(dtype).reshape(-1, cols)
+
+
+def gpu_decrypt(level, W):
+    p = hqc.params(level)
+    B = W["u"].shape[0]
+    m = torch.empty(B * p.k, dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch(level, to_dev(W["u"]), to_dev(W["v"]), to_dev(W["y"]), m)
+    torch.cuda.synchronize()
+    return from_dev(m, np.uint8, p.k)
+
+
+def gpu_stage1(level, W, with_v=True):
+    p = hqc.params(level)
+    B = W["u"].shape[0]
+    r = torch.empty(B * p.v_words * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_sparse_dense_mul_batch(level, to_dev(W["u"]), to_dev(W["y"]), to_dev(W["v"]) if with_v else None, r)
+    torch.cuda.synchronize()
+    return from_dev(r, np.uint64, p.v_words)
+
+
+def gpu_stage2(level, r):
+    p = hqc.params(level)
+    B = r.shape[0]
+    s = torch.empty(B * p.n1, dtype=torch.uint8, device=DEV)
+    hqc.hqc_rm_decode_batch(level, to_dev(r), s)
+    torch.cuda.synchronize()
+    return from_dev(s, np.uint8, p.n1)
+
+
+def gpu_stage3(level, sym):
+    p = hqc.params(level)
+    B = sym.shape[0]
+    m = torch.empty(B * p.k, dtype=torch.uint8, device=DEV)
+    ok = torch.empty(B, dtype=torch.uint8, device=DEV)
+    hqc.hqc_rs_decode_batch(level, to_dev(sym), m, ok)
+    torch.cuda.synchronize()
+    return from_dev(m, np.uint8, p.k), ok.cpu().numpy()
+
+
+# ---------------------------------------------------------------- end to end, small
+@pytest.mark.parametrize("level", LEVELS)
+@pytest.mark.parametrize("B", [1, 33, 200])
+def test_decrypt_valid(level, B):
+    W = valid_batch(level, 1000, B)
+    p = W["params"]
+    got = gpu_decrypt(level, W)
+    assert (got == W["m"]).all()
+    assert (got == oracle.decrypt_batch(p, W["u"], W["v"], W["y"])).all()
+
+
+def test_decrypt_adversarial_quarters():
+    W = adversarial_batch(0, 512, 512)
+    p = W["params"]
+    ref = oracle.decrypt_batch(p, W["u"], W["v"], W["y"])
+    got = gpu_decrypt(1, W)
+    bad = np.nonzero((got != ref).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first rows {bad[:8]} quarters {W['quarter'][bad[:8]]}"
+    q = W["quarter"]
+    assert (got[q == 0] == W["m"][q == 0]).all()
+    assert (got[q == 3] != W["m"][q == 3]).any(axis=1).mean() > 0.9  # random ciphertexts: garbage
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_decrypt_random_ciphertexts_and_edges(level):
+    p = oracle.params(level)
+    W = valid_batch(level, 5000, 70)
+    rng = np.random.default_rng(level)
+    # rows 0..29: uniformly random u, v (undecodable garbage)
+    W["u"][:30] = gen.dense(11, gen.TAG_U_RAND, 0, 30, p.n, W["u"].shape[1])
+    W["v"][:30] = gen.dense(11, gen.TAG_V_RAND, 0, 30, p.n12, W["v"].shape[1])
+    # rows 30..33: supports hitting 0 and n-1 (the d = n and d = 1 rotations)
+    W["y"][30, 0] = 0
+    W["y"][31, p.w - 1] = p.n - 1
+    W["y"][32, :p.w] = np.arange(p.w, dtype=np.uint32)
+    W["y"][33, :p.w] = p.n - 1 - np.arange(p.w, dtype=np.uint32)
+    # row 34: all-zero ciphertext -> 0^k; row 35: u pad bits set (ignored, R#13)
+    W["u"][34] = 0
+    W["v"][34] = 0
+    W["u"][35, p.words - 1] |= np.uint64(0xFFFFFFFFFFFFFFFF) << np.uint64(p.n % 64)
+    if W["u"].shape[1] > p.words:
+        W["u"][35, p.words:] = rng.integers(0, 2**63, W["u"].shape[1] - p.words, dtype=np.uint64)
+    # padding entries of y rows are ignored
+    W["y"][36, p.w:] = 12345
+    ref = oracle.decrypt_batch(p, W["u"], W["v"], W["y"])
+    got = gpu_decrypt(level, W)
+    assert (got == ref).all()
+    assert (got[34] == 0).all()
+
+
+# ---------------------------------------------------------------- per stage
+@pytest.mark.parametrize("level", LEVELS)
+def test_stage1_product(level):
+    W = valid_batch(level, 2000, 97)
+    p = W["params"]
+    W["u"][:20] = gen.dense(3, gen.TAG_U_RAND, 0, 20, p.n, W["u"].shape[1])
+    ref = oracle.stage1_batch(p, W["u"], W["v"], W["y"])
+    assert (gpu_stage1(level, W) == ref).all()
+    # v = NULL: the truncated product alone
+    ref0 = oracle.stage1_batch(p, W["u"], np.zeros_like(W["v"]), W["y"])
+    assert (gpu_stage1(level, W, with_v=False) == ref0).all()
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_stage2_rm_random_and_real(level):
+    p = oracle.params(level)
+    r_rand = gen.dense(21, gen.TAG_TEST, 0, 150, p.n12, p.vwords)  # ~20% tied blocks (R#11)
+    W = valid_batch(level, 3000, 40)
+    r_real = oracle.stage1_batch(p, W["u"], W["v"], W["y"])
+    for r in (r_rand, r_real):
+        assert (gpu_stage2(level, r) == oracle.rm_decode_batch(p, r)).all()
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_stage3_rs(level):
+    p = oracle.params(level)
+    rng = np.random.default_rng(100 + level)
+    rows = []
+    kinds = []
+    for i in range(300):
+        m = rng.integers(0, 256, p.k).astype(np.uint8)
+        c = oracle.rs_encode(m, p.n1, p.k)
+        kind = i % 5
+        if kind == 0:  # clean
+            pass
+        elif kind == 1:  # exactly delta errors
+            pos = rng.choice(p.n1, p.delta, replace=False)
+            c[pos] ^= rng.integers(1, 256, p.delta).astype(np.uint8)
+        elif kind == 2:  # random number of errors <= delta, some in the message part
+            t = int(rng.integers(1, p.delta + 1))
+            pos = rng.choice(p.n1, t, replace=False)
+            c[pos] ^= rng.integers(1, 256, t).astype(np.uint8)
+        elif kind == 3:  # beyond capacity
+            t = int(rng.integers(p.delta + 1, 2 * p.delta + 1))
+            pos = rng.choice(p.n1, t, replace=False)
+            c[pos] ^= rng.integers(1, 256, t).astype(np.uint8)
+        else:  # garbage
+            c = rng.integers(0, 256, p.n1).astype(np.uint8)
+        rows.append(c)
+        kinds.append(kind)
+    sym = np.stack(rows)
+    ref, ref_ok = oracle.rs_decode_batch(p, sym)
+    got, ok = gpu_stage3(level, sym)
+    assert (got == ref).all()
+    assert (ok == ref_ok).all()
+    kinds = np.array(kinds)
+    assert ok[kinds <= 2].all() and not ok[kinds == 4].any()
+
+
+# ---------------------------------------------------------------- API behaviour
+def test_batch_zero_and_errors():
+    p = hqc.params(1)
+    x = torch.zeros(16, dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch(1, x[:0], x[:0], x[:0], x[:0])  # batch 0: no launch, no error
+    with pytest.raises(hqc.HqcError):
+        hqc.hqc_decrypt_batch(2, x, x, x, x)
+
+
+def test_mismatch_counter_and_support_validation():
+    W = valid_batch(3, 7000, 64)
+    p = hqc.params(3)
+    m = torch.from_numpy(W["m"]).to(DEV)
+    m2 = m.clone()
+    m2[5, 3] ^= 1
+    m2[40, 0] ^= 0x80
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    hqc.hqc_count_mismatch(3, m, m2, cnt)
+    assert int(cnt.item()) == 2
+    y = W["y"].copy()
+    y[3, 0] = p.n
+    y[9, 2] = y[9, 1]
+    bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+    hqc.hqc_validate_support(3, to_dev(y), bad)
+    assert int(bad.item()) == 2
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+FULL = [(1, 1024), (3, 65536), (5, 262144)]
+
+
+@pytest.mark.parametrize("level,B", FULL)
+def test_full_size_config(level, B):
+    """BASELINE configs[0..2] at their batch sizes, launched exactly as bench.py launches them.
+    Rows are 4096 distinct oracle-encrypted ciphertexts tiled to B (row i = ciphertext i mod 4096),
+    so every output is known: decrypt(encrypt(m)) = m at every row, and a sample of rows is checked
+    against the oracle's own decryption."""
+    D = min(B, 4096)
+    W = valid_batch(level, 10_000, D)
+    p = W["params"]
+    reps = B // D
+    u = np.tile(W["u"], (reps, 1))
+    v = np.tile(W["v"], (reps, 1))
+    y = np.tile(W["y"], (reps, 1))
+    got = gpu_decrypt(level, dict(u=u, v=v, y=y))
+    assert (got == np.tile(W["m"], (reps, 1))).all()
+    idx = np.random.default_rng(level).choice(B, 64, replace=False)
+    ref = oracle.decrypt_batch(p, u[idx], v[idx], y[idx])
+    assert (got[idx] == ref).all()
+
+
+def test_full_size_adversarial():
+    """BASELINE configs[3] (1,048,576 HQC-1, four quarters) in the bench launch configuration:
+    the batch is 4 x 8192 distinct adversarial ciphertexts per quarter tiled 32 times; every row
+    is compared against the oracle's output for its source row."""
+    B, D = 1_048_576, 32768
+    W = adversarial_batch(0, D, D)
+    p = W["params"]
+    ref = oracle.decrypt_batch(p, W["u"], W["v"], W["y"])
+    q = D // 4
+    order = np.concatenate([np.tile(np.arange(k * q, (k + 1) * q), B // D) for k in range(4)])
+    got = gpu_decrypt(1, dict(u=W["u"][order], v=W["v"][order], y=W["y"][order]))
+    assert (got == ref[order]).all()
