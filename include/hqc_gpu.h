@@ -116,6 +116,25 @@ int hqc_count_mismatch(const hqc_params *p, const uint8_t *m_out, const uint8_t 
 int hqc_validate_support(const hqc_params *p, const uint32_t *y_support, size_t batch,
                          unsigned long long *d_bad, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * the KeyGen product and batched Encrypt on the GPU (used by bench.py to
+ * build valid ciphertexts on the device; parity-tested against the oracle).
+ * hqc_keygen_batch (Alg. 3):  s[i] = x[i] + h[i]*y[i]
+ *   h [nkeys][u_stride] uint64 (bits >= n ignored), x, y [nkeys][y_stride] uint32 (first w used),
+ *   s_out [nkeys][u_stride] uint64 (bits >= n and padding words written as zero).
+ * hqc_encrypt_batch (Alg. 1):  u = r1 + h*r2,  v = trunc_{n1 n2}(mG + s*r2 + e)
+ *   h, s [nkeys][u_stride] (the public key of each ciphertext, rows selected by key_index[b], or row b
+ *   when key_index is NULL), m [batch][k], r1, r2, e [batch][e_stride] uint32 (first wr used, distinct,
+ *   < n), u_out [batch][u_stride], v_out [batch][v_words]. mG is the concatenated RS/RM encoding of m
+ *   (message-first RS by the table-driven LFSR of §III.D, duplicated RM(1,7) per R#9/R#12).
+ * ------------------------------------------------------------------------------------------- */
+int hqc_keygen_batch(const hqc_params *p, const uint64_t *h, const uint32_t *x, const uint32_t *y,
+                     uint64_t *s_out, size_t nkeys, void *stream);
+int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
+                      const uint32_t *key_index, const uint8_t *m, const uint32_t *r1,
+                      const uint32_t *r2, const uint32_t *e, uint64_t *u_out, uint64_t *v_out,
+                      size_t batch, void *stream);
+
 /* Number of persistent CTAs / warps the fused kernel launches for `batch` on the current device
  * (introspection for the bench's launch accounting). Returns HQC_OK. */
 int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);

@@ -1,0 +1,226 @@
+// batched HQC.PKE.Encrypt (Alg. 1) and the KeyGen product
+// (Alg. 3) on the GPU, reusing the stage-1 sparse x dense machinery with full-width
+// outputs. Used by bench.py to make valid ciphertexts on the device; parity-tested against the
+// oracle's encrypt/keygen in tests/test_gpu_encrypt.py.
+//
+//   keygen:  s = x + h*y                       (n bits, pad bits zero)
+//   encrypt: u = r1 + h*r2                     (n bits, pad bits zero)
+//            v = trunc_{n1 n2}(mG + s*r2 + e)  mG = RM(1,7)^mult o RS(message-first)   (R#3, R#6, R#9)
+// The RS encoder is the paper's table-driven LFSR (§III.D, Fig. "rs_lookup_table"): a
+// constant table T[f][t] = g*_t * f (2delta x 256 bytes, "approximately 8 KB" for HQC-1) turns every
+// per-byte GF multiply into a lookup; g* is the reciprocal generator (message-first layout, R#6).
+#pragma once
+#include <cstdint>
+
+#include "levels.cuh"
+#include "stage1.cuh"
+
+namespace hqc {
+
+// ---- compile-time RS generator tables -------------------------------------------------------------
+constexpr uint32_t gf_mul_c(uint32_t a, uint32_t b) {  // carry-less product mod 0x11D (compile time)
+  uint32_t r = 0;
+  for (int i = 0; i < 8; i++)
+    if ((b >> i) & 1) r ^= a << i;
+  for (int d = 14; d >= 8; d--)
+    if ((r >> d) & 1) r ^= 0x11Du << (d - 8);
+  return r;
+}
+constexpr uint32_t gf_pow_c(uint32_t a, uint32_t e) {
+  uint32_t r = 1;
+  for (uint32_t i = 0; i < e; i++) r = gf_mul_c(r, a);
+  return r;
+}
+
+template <uint32_t TD> struct RsEncTable {
+  uint8_t t[256][TD];  // t[f][j] = g*_j * f
+};
+// g*(x) = prod_{i=1}^{2delta} (x + alpha^{-i}) = prod (x + alpha^{255-i}); coefficients g*_0..g*_{2delta-1}
+template <uint32_t TD> constexpr RsEncTable<TD> make_rs_enc_table() {
+  uint32_t g[TD + 1] = {};
+  g[0] = 1;
+  for (uint32_t i = 1; i <= TD; i++) {
+    const uint32_t root = gf_pow_c(2, 255 - i);
+    for (uint32_t t = i; t > 0; t--) g[t] = g[t - 1] ^ gf_mul_c(g[t], root);
+    g[0] = gf_mul_c(g[0], root);
+  }
+  RsEncTable<TD> T{};
+  for (uint32_t f = 0; f < 256; f++)
+    for (uint32_t j = 0; j < TD; j++) T.t[f][j] = static_cast<uint8_t>(gf_mul_c(g[j], f));
+  return T;
+}
+__device__ const RsEncTable<30> c_rs_enc30 = make_rs_enc_table<30>();
+__device__ const RsEncTable<32> c_rs_enc32 = make_rs_enc_table<32>();
+__device__ const RsEncTable<58> c_rs_enc58 = make_rs_enc_table<58>();
+template <uint32_t TD> __device__ __forceinline__ const uint8_t (*rs_table())[TD];
+template <> __device__ __forceinline__ const uint8_t (*rs_table<30>())[30] { return c_rs_enc30.t; }
+template <> __device__ __forceinline__ const uint8_t (*rs_table<32>())[32] { return c_rs_enc32.t; }
+template <> __device__ __forceinline__ const uint8_t (*rs_table<58>())[58] { return c_rs_enc58.t; }
+
+// Warp-cooperative systematic RS encode of k message bytes (smem msg) into cw[0..n1) (smem).
+// Lane t holds LFSR cells t and t+32. c_j = m_j (j < k); c_{n1-1-e} = remainder coefficient e.
+template <class P>
+__device__ __forceinline__ void rs_encode_warp(const uint8_t *msg, uint8_t *cw, int lane) {
+  constexpr uint32_t TD = P::TWO_DELTA;
+  const uint8_t(*T)[TD] = rs_table<TD>();
+  uint32_t A = 0, B = 0;  // cells lane and lane + 32
+  for (uint32_t j = 0; j < P::K; j++) {
+    const uint32_t top = (TD - 1 < 32) ? __shfl_sync(0xffffffffu, A, TD - 1) : __shfl_sync(0xffffffffu, B, TD - 1 - 32);
+    const uint32_t fb = msg[j] ^ top;
+    const uint32_t upA = __shfl_up_sync(0xffffffffu, A, 1);
+    const uint32_t upB = __shfl_up_sync(0xffffffffu, B, 1);
+    const uint32_t a31 = __shfl_sync(0xffffffffu, A, 31);
+    const uint32_t nA = (lane == 0 ? 0u : upA) ^ ((uint32_t)lane < TD ? T[fb][lane] : 0u);
+    const uint32_t nB = (lane == 0 ? a31 : upB) ^ ((uint32_t)lane + 32 < TD ? T[fb][lane + 32] : 0u);
+    A = nA;
+    B = (uint32_t)lane + 32 < TD ? nB : 0u;
+  }
+  for (uint32_t j = lane; j < P::K; j += 32) cw[j] = msg[j];
+  if ((uint32_t)lane < TD) cw[P::N1 - 1 - lane] = (uint8_t)A;
+  if ((uint32_t)lane + 32 < TD) cw[P::N1 - 1 - (lane + 32)] = (uint8_t)B;
+}
+
+// The 128-bit RM(1,7) codeword of byte b (R#9): bit p = b7 ^ parity(b & 0x7F & p), word q = p >> 5.
+__device__ __forceinline__ void rm_encode_byte(uint32_t b, uint32_t (&w)[4]) {
+  const uint32_t rows[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
+  uint32_t base = (b & 0x80u) ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+  for (int t = 0; t < 5; t++) base ^= ((b >> t) & 1u) ? rows[t] : 0u;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t flip = (((b >> 5) & 1u) & (q & 1)) ^ (((b >> 6) & 1u) & (q >> 1));
+    w[q] = base ^ (flip ? 0xFFFFFFFFu : 0u);
+  }
+}
+
+// Coalesced copy of nwords (multiple of 4) 32-bit words global -> shared.
+__device__ __forceinline__ void copy_g2s(uint32_t *dst, const void *src, uint32_t nwords, int lane) {
+  const uint4 *s = reinterpret_cast<const uint4 *>(src);
+  for (uint32_t c = lane; c < nwords / 4; c += 32) reinterpret_cast<uint4 *>(dst)[c] = __ldg(s + c);
+}
+__device__ __forceinline__ void copy_s2g(void *dst, const uint32_t *src, uint32_t nwords, int lane) {
+  uint4 *d = reinterpret_cast<uint4 *>(dst);
+  for (uint32_t c = lane; c < nwords / 4; c += 32) d[c] = reinterpret_cast<const uint4 *>(src)[c];
+}
+
+// One warp: out (NOUT words in smem, aliasing E) = dense (staged in su) * support (staged in ssup)
+template <class P, class S>
+__device__ __forceinline__ void warp_product(const uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
+                                             int lane) {
+  s1_stage_d<P, S>(ssup, dsm, lane);
+  s1_build_E<P, S>(su, E, lane);
+  __syncwarp();
+  uint32_t acc[S::R];
+  s1_product<P, S>(E, dsm, acc, lane);
+  __syncwarp();
+  s1_store_r<S>(acc, E, lane);
+  __syncwarp();
+}
+
+// XOR the bits of a support (first wt entries, positions < limit) into a bit vector in smem.
+__device__ __forceinline__ void xor_support_bits(uint32_t *vec, const uint32_t *supp, uint32_t wt, uint32_t limit,
+                                                 int lane) {
+  for (uint32_t j = lane; j < wt; j += 32) {
+    const uint32_t p = supp[j];
+    if (p < limit) atomicXor(vec + (p >> 5), 1u << (p & 31));
+  }
+}
+
+template <class P> struct EncSmem {
+  static constexpr uint32_t EW = FullShape<P>::E_WORDS > EncVShape<P>::E_WORDS ? FullShape<P>::E_WORDS
+                                                                               : EncVShape<P>::E_WORDS;
+  static constexpr uint32_t E_BYTES = round_up(EW * 4, 16);
+  static constexpr uint32_t STG_BYTES = round_up(P::U_STRIDE * 8, 16);
+  static constexpr uint32_t SUP_BYTES = round_up(P::E_STRIDE * 4, 16) * 3;  // r1/x, r2/y, e
+  static constexpr uint32_t D_BYTES = round_up(round_up(P::WR, 4) * 4, 16);
+  static constexpr uint32_t MISC_BYTES = round_up(P::N1 + P::K + 16, 16);
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + SUP_BYTES + D_BYTES + MISC_BYTES;
+};
+
+// keygen: s[k] = x[k] + h[k]*y[k]. One warp per key.
+template <class P>
+__global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, const uint32_t *__restrict__ x,
+                                               const uint32_t *__restrict__ y, uint64_t *__restrict__ s, size_t nkeys) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using M = EncSmem<P>;
+  using S = KeyShape<P>;
+  const int lane = threadIdx.x;
+  uint32_t *E = reinterpret_cast<uint32_t *>(smem);
+  uint32_t *stg = reinterpret_cast<uint32_t *>(smem + M::E_BYTES);
+  uint32_t *sx = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_BYTES);
+  uint32_t *sy = sx + M::SUP_BYTES / 12;
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_BYTES + M::SUP_BYTES);
+  for (size_t kk = blockIdx.x; kk < nkeys; kk += gridDim.x) {
+    copy_g2s(stg, h + kk * P::U_STRIDE, 2 * P::U_STRIDE, lane);
+    copy_g2s(sx, x + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
+    copy_g2s(sy, y + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
+    __syncwarp();
+    warp_product<P, S>(stg, sy, E, dsm, lane);
+    xor_support_bits(E, sx, P::W, P::N, lane);
+    __syncwarp();
+    if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;  // bits >= n are zero
+    for (uint32_t q = P::Q0 + 1 + lane; q < 2 * P::U_STRIDE; q += 32) E[q] = 0;
+    __syncwarp();
+    copy_s2g(s + kk * P::U_STRIDE, E, 2 * P::U_STRIDE, lane);
+    __syncwarp();
+  }
+}
+
+// encrypt: one warp per ciphertext.
+template <class P>
+__global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
+                                                const uint32_t *__restrict__ key_index, const uint8_t *__restrict__ m,
+                                                const uint32_t *__restrict__ r1, const uint32_t *__restrict__ r2,
+                                                const uint32_t *__restrict__ e, uint64_t *__restrict__ u_out,
+                                                uint64_t *__restrict__ v_out, size_t batch) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using M = EncSmem<P>;
+  const int lane = threadIdx.x;
+  uint32_t *E = reinterpret_cast<uint32_t *>(smem);
+  uint32_t *stg = reinterpret_cast<uint32_t *>(smem + M::E_BYTES);
+  uint32_t *s_r1 = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_BYTES);
+  uint32_t *s_r2 = s_r1 + M::SUP_BYTES / 12;
+  uint32_t *s_e = s_r2 + M::SUP_BYTES / 12;
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_BYTES + M::SUP_BYTES);
+  uint8_t *cw = smem + M::E_BYTES + M::STG_BYTES + M::SUP_BYTES + M::D_BYTES;
+  uint8_t *msg = cw + P::N1;
+  for (size_t ct = blockIdx.x; ct < batch; ct += gridDim.x) {
+    const size_t key = key_index ? key_index[ct] : ct;
+    copy_g2s(s_r1, r1 + ct * P::E_STRIDE, P::E_STRIDE, lane);
+    copy_g2s(s_r2, r2 + ct * P::E_STRIDE, P::E_STRIDE, lane);
+    copy_g2s(s_e, e + ct * P::E_STRIDE, P::E_STRIDE, lane);
+    copy_g2s(stg, h + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
+    for (uint32_t j = lane; j < P::K; j += 32) msg[j] = m[ct * P::K + j];
+    __syncwarp();
+    // u = r1 + h * r2 (all n bits)
+    warp_product<P, FullShape<P>>(stg, s_r2, E, dsm, lane);
+    xor_support_bits(E, s_r1, P::WR, P::N, lane);
+    __syncwarp();
+    if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;
+    for (uint32_t q = P::Q0 + 1 + lane; q < 2 * P::U_STRIDE; q += 32) E[q] = 0;
+    __syncwarp();
+    copy_s2g(u_out + ct * P::U_STRIDE, E, 2 * P::U_STRIDE, lane);
+    __syncwarp();
+    // v = trunc(mG + s * r2 + e)
+    copy_g2s(stg, s + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
+    rs_encode_warp<P>(msg, cw, lane);
+    __syncwarp();
+    warp_product<P, EncVShape<P>>(stg, s_r2, E, dsm, lane);
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // RM-encode symbol j into block j, every copy
+      uint32_t w[4];
+      rm_encode_byte(cw[j], w);
+      uint32_t *blk = E + j * (P::N2 / 32);
+#pragma unroll
+      for (uint32_t c = 0; c < P::MULT; c++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) blk[4 * c + q] ^= w[q];
+    }
+    __syncwarp();
+    xor_support_bits(E, s_e, P::WR, P::N12, lane);
+    __syncwarp();
+    copy_s2g(v_out + ct * P::V_WORDS, E, P::NW, lane);
+    __syncwarp();
+  }
+}
+
+}  // namespace hqc

@@ -6,6 +6,8 @@
 #include <mutex>
 
 #include "../../include/hqc_gpu.h"
+#include "async_copy.cuh"
+#include "encrypt.cuh"
 #include "gf256.cuh"
 #include "levels.cuh"
 #include "stage1.cuh"
@@ -18,11 +20,80 @@ namespace hqc {
 // Shared-memory carve-up of the fused / stage-1 kernels (per warp), 16-byte aligned pieces.
 template <class P> struct WarpSmem {
   static constexpr uint32_t E_BYTES = round_up(
-      (P::E_WORDS * 4 > S3Scratch<P>::BYTES ? P::E_WORDS * 4 : S3Scratch<P>::BYTES), 16);
-  static constexpr uint32_t D_BYTES = round_up(P::WPAD * 4, 16);
+      (DecShape<P>::E_WORDS * 4 > S3Scratch<P>::BYTES ? DecShape<P>::E_WORDS * 4 : S3Scratch<P>::BYTES), 16);
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static_assert(UB % 16 == 0 && VB % 16 == 0 && YB % 16 == 0, "TMA bulk copies move 16-byte multiples");
+  static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
+  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(DecShape<P>::WPAD * 4, 16);
   static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 32, 16);
-  static constexpr uint32_t BYTES = E_BYTES + D_BYTES + SYM_BYTES;
+  static constexpr uint32_t BAR_BYTES = 16;
+  static constexpr uint32_t S1_BYTES = E_BYTES + STG_BYTES + D_BYTES + BAR_BYTES;  // stage-1 kernel
+  static constexpr uint32_t BYTES = S1_BYTES + SYM_BYTES;                          // fused kernel
 };
+
+// Per-warp stage-1 pipeline: rows of ciphertext i+1 are fetched by TMA while ciphertext i is
+// computed (u and y during stage 2/3 of ciphertext i, v during its product loop).
+template <class P> struct S1Pipe {
+  uint32_t *E, *stg_u, *stg_y, *dsm;
+  uint64_t *bar;
+  uint32_t phase;
+  const uint64_t *u, *v;
+  const uint32_t *y;
+
+  __device__ __forceinline__ S1Pipe(uint8_t *ws, const uint64_t *u_, const uint64_t *v_, const uint32_t *y_, int lane)
+      : u(u_), v(v_), y(y_) {
+    using S = WarpSmem<P>;
+    E = reinterpret_cast<uint32_t *>(ws);
+    stg_u = reinterpret_cast<uint32_t *>(ws + S::E_BYTES);
+    stg_y = reinterpret_cast<uint32_t *>(ws + S::E_BYTES + S::STG_UV_BYTES);
+    dsm = reinterpret_cast<uint32_t *>(ws + S::E_BYTES + S::STG_BYTES);
+    bar = reinterpret_cast<uint64_t *>(ws + S::E_BYTES + S::STG_BYTES + S::D_BYTES);
+    phase = 0;
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+  }
+  __device__ __forceinline__ void wait() {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+  }
+  __device__ __forceinline__ void issue_uy(size_t ct, int lane) {
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, WarpSmem<P>::UB + WarpSmem<P>::YB);
+      tma_load_1d(stg_u, u + ct * P::U_STRIDE, WarpSmem<P>::UB, bar);
+      tma_load_1d(stg_y, y + ct * P::Y_STRIDE, WarpSmem<P>::YB, bar);
+    }
+  }
+  __device__ __forceinline__ void issue_v(size_t ct, int lane) {
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, WarpSmem<P>::VB);
+      tma_load_1d(stg_u, v + ct * P::V_WORDS, WarpSmem<P>::VB, bar);
+    }
+  }
+  // Stage 1 of ciphertext ct (its u, y already requested); leaves r in E; requests next's u, y.
+  __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
+    wait();
+    using S = DecShape<P>;
+    s1_stage_d<P, S>(stg_y, dsm, lane);
+    s1_build_E<P, S>(stg_u, E, lane);
+    __syncwarp();
+    if (v) issue_v(ct, lane);
+    uint32_t acc[S::R];
+    s1_product<P, S>(E, dsm, acc, lane);
+    __syncwarp();  // every lane is done reading E: r overwrites it
+    s1_store_r<S>(acc, E, lane);
+    __syncwarp();
+    if (v) {
+      wait();
+      s1_xor_v<P::NW>(E, stg_u, lane);
+      __syncwarp();
+    }
+    if (has_next) issue_uy(next, lane);
+  }
+};
+
 constexpr uint32_t GF_BYTES = round_up(sizeof(GfTables), 16);
 
 // ------------------------------------------------------------------------------------------------
@@ -33,14 +104,14 @@ __global__ void __launch_bounds__(128) k_stage1(const uint64_t *__restrict__ u, 
                                                 size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t *ws = smem + (size_t)wib * (WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES);
-  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
-  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + WarpSmem<P>::E_BYTES);
+  S1Pipe<P> pipe(smem + (size_t)wib * WarpSmem<P>::S1_BYTES, u, v, y, lane);
   const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
-  for (size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib; ct < batch; ct += nwarps) {
-    s1_run<P>(u + ct * P::U_STRIDE, y + ct * P::Y_STRIDE, v ? v + ct * P::V_WORDS : nullptr, E, dsm, lane);
+  size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (ct < batch) pipe.issue_uy(ct, lane);
+  for (; ct < batch; ct += nwarps) {
+    pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
     uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
-    const uint4 *src = reinterpret_cast<const uint4 *>(E);
+    const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E);
     for (uint32_t c = lane; c < P::NW / 4; c += 32) dst[c] = src[c];
     __syncwarp();
   }
@@ -105,19 +176,19 @@ __global__ void __launch_bounds__(128) k_decrypt(const uint64_t *__restrict__ u,
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t *ws = smem + GF_BYTES + (size_t)wib * WarpSmem<P>::BYTES;
-  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
-  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + WarpSmem<P>::E_BYTES);
-  uint8_t *sb = ws + WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES;
+  S1Pipe<P> pipe(ws, u, v, y, lane);
+  uint8_t *sb = ws + WarpSmem<P>::S1_BYTES;
   const size_t g = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const size_t lo = g * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
+  if (lo < hi) pipe.issue_uy(lo, lane);
   for (size_t base = lo; base < hi; base += 32) {
     const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
     for (uint32_t s = 0; s < rows; s++) {
       const size_t ct = base + s;
-      s1_run<P>(u + ct * P::U_STRIDE, y + ct * P::Y_STRIDE, v + ct * P::V_WORDS, E, dsm, lane);
+      pipe.run(ct, ct + 1 < hi, ct + 1, lane);
       for (uint32_t j = lane; j < P::N1; j += 32) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(E) + j * (P::N2 / 128);
+        const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
         uint32_t X[P::MULT * 4];
 #pragma unroll
         for (int c = 0; c < (int)P::MULT; c++) {
@@ -133,7 +204,8 @@ __global__ void __launch_bounds__(128) k_decrypt(const uint64_t *__restrict__ u,
     __syncwarp();
     const bool act = (uint32_t)lane < rows;
     auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
-    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(E), lane, act ? m_out + (base + lane) * P::K : nullptr);
+    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
+                      act ? m_out + (base + lane) * P::K : nullptr);
     __syncwarp();
   }
 }
@@ -179,9 +251,7 @@ static DevInfo g_dev[16];
 constexpr int WARPS_PER_CTA = 1;  // fused / stage-1 kernels: one warp per CTA (fine-grained SM balance)
 
 template <class P> static uint32_t decrypt_smem() { return GF_BYTES + WARPS_PER_CTA * WarpSmem<P>::BYTES; }
-template <class P> static uint32_t stage1_smem() {
-  return WARPS_PER_CTA * (WarpSmem<P>::E_BYTES + WarpSmem<P>::D_BYTES);
-}
+template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }
@@ -210,9 +280,12 @@ static int cur_device(DevInfo **out) {
   return dev;
 }
 
+// Work split of the fused kernel: every resident warp gets an equal contiguous range (at least
+// MIN_PER ciphertexts, so the lane-per-ciphertext RS stage keeps most lanes busy).
+constexpr size_t MIN_PER = 16;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
   const size_t cap = (size_t)di.sms * di.cap_decrypt[P::level] * WARPS_PER_CTA;
-  size_t warps = (batch + 31) / 32;
+  size_t warps = (batch + MIN_PER - 1) / MIN_PER;
   if (warps > cap) warps = cap;
   if (warps == 0) warps = 1;
   *per = (batch + warps - 1) / warps;
@@ -263,6 +336,35 @@ static int launch_stage3(const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t bat
   const size_t cap = (size_t)di->sms * 16;
   if (grid > cap) grid = cap;
   k_stage3<P><<<(unsigned)grid, 32 * warps, stage3_smem<P>(warps), st>>>(sym, m, ok, batch);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_keygen(const uint64_t *h, const uint32_t *x, const uint32_t *y, uint64_t *s, size_t nkeys,
+                         cudaStream_t st) {
+  const uint32_t smem = EncSmem<P>::BYTES;
+  if (cudaFuncSetAttribute(k_keygen<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return HQC_ERR_CUDA;
+  size_t grid = nkeys < 65535 ? nkeys : 65535;
+  k_keygen<P><<<(unsigned)grid, 32, smem, st>>>(h, x, y, s, nkeys);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_encrypt(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m,
+                          const uint32_t *r1, const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v,
+                          size_t batch, cudaStream_t st) {
+  const uint32_t smem = EncSmem<P>::BYTES;
+  if (cudaFuncSetAttribute(k_encrypt<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return HQC_ERR_CUDA;
+  DevInfo *di;
+  if (cur_device(&di) < 0) return HQC_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  size_t grid = batch;
+  const size_t cap = (size_t)(sms > 0 ? sms : 148) * 16;
+  if (grid > cap) grid = cap;
+  k_encrypt<P><<<(unsigned)grid, 32, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
@@ -408,4 +510,28 @@ extern "C" int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *
   if (s) return s;
   if (!grid || !wpc) return HQC_ERR_NULL;
   HQC_DISPATCH(p, shape_impl, batch, grid, wpc);
+}
+
+extern "C" int hqc_keygen_batch(const hqc_params *p, const uint64_t *h, const uint32_t *x, const uint32_t *y,
+                                uint64_t *s_out, size_t nkeys, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (nkeys == 0) return HQC_OK;
+  if (nkeys > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(h); HQC_CHECK_PTR(x); HQC_CHECK_PTR(y); HQC_CHECK_PTR(s_out);
+  HQC_DISPATCH(p, launch_keygen, h, x, y, s_out, nkeys, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
+                                 const uint32_t *key_index, const uint8_t *m, const uint32_t *r1,
+                                 const uint32_t *r2, const uint32_t *e, uint64_t *u_out, uint64_t *v_out,
+                                 size_t batch, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(h); HQC_CHECK_PTR(s); HQC_CHECK_PTR(m); HQC_CHECK_PTR(r1); HQC_CHECK_PTR(r2);
+  HQC_CHECK_PTR(e); HQC_CHECK_PTR(u_out); HQC_CHECK_PTR(v_out);
+  if (key_index && misaligned(key_index)) return HQC_ERR_ALIGN;
+  HQC_DISPATCH(p, launch_encrypt, h, s, key_index, m, r1, r2, e, u_out, v_out, batch, (cudaStream_t)stream);
 }

@@ -27,20 +27,29 @@ template <int LEVEL> struct Lv : Table1<LEVEL> {
   static constexpr uint32_t V_WORDS = N12 / 64;
   static constexpr uint32_t Y_STRIDE = round_up(W, 4);
   static constexpr uint32_t E_STRIDE = round_up(WR, 4);
-  // stage 1: a warp owns one ciphertext; lane L owns R consecutive 32-bit output
-  // words [L*R, L*R+R). R is odd so that the 32 lanes' shared-memory reads E[o + L*R + k] fall in 32
-  // distinct banks for every (o, k).
-  static constexpr uint32_t R = make_odd_up((NW + 31) / 32);
   static constexpr uint32_t Q0 = N / 32;               // word holding bit n-1
   static constexpr uint32_t C = N % 32;                // bits of u in word Q0 (nonzero: n is prime)
-  // E[b] = u[b mod n] for b < 32*E_WORDS: the "doubled" u, so every rotation is a plain funnel shift
-  static constexpr uint32_t E_WORDS = round_up(Q0 + 32 * R + 2, 4);
-  static constexpr uint32_t WPAD = round_up(W, 4);     // d-values staged per warp
   static_assert(C != 0, "n must not be a multiple of 32");
   static_assert(N12 % 128 == 0, "r is processed in 16-byte chunks");
   static_assert(N2 % 128 == 0 && (N2 / 32) % 4 == 0, "RM blocks are whole 16-byte chunks");
   static_assert(N1 - K == TWO_DELTA, "shortened RS: n1 - k = 2 delta");
   static_assert(K <= 32, "Forney root flags for message positions fit one 32-bit mask");
 };
+
+// Shape of one warp-level sparse x dense product (stage1.cuh): NOUT 32-bit output words, a sparse
+// operand of weight WT. A warp owns one product; lane L owns R consecutive output words
+// [L*R, L*R+R). R is odd so that the 32 lanes' shared-memory reads E[o + L*R + k] fall in 32
+// distinct banks for every (o, k). E[b] = u[b mod n] for b < 32*E_WORDS: the "doubled" dense
+// operand, so every rotation is a plain funnel shift.
+template <class P, uint32_t NOUT_, uint32_t WT_> struct ProdShape {
+  static constexpr uint32_t NOUT = NOUT_, WT = WT_;
+  static constexpr uint32_t R = make_odd_up((NOUT + 31) / 32);
+  static constexpr uint32_t E_WORDS = round_up(P::Q0 + 32 * R + 2, 4);
+  static constexpr uint32_t WPAD = round_up(WT, 4);
+};
+template <class P> using DecShape = ProdShape<P, P::NW, P::W>;          // u*y truncated to n1*n2 bits
+template <class P> using FullShape = ProdShape<P, P::Q0 + 1, P::WR>;    // h*r2: all n bits
+template <class P> using KeyShape = ProdShape<P, P::Q0 + 1, P::W>;      // h*y: all n bits
+template <class P> using EncVShape = ProdShape<P, P::NW, P::WR>;        // s*r2 truncated
 
 }  // namespace hqc

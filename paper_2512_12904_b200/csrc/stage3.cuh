@@ -30,11 +30,13 @@ __device__ __forceinline__ uint32_t mod255_add(uint32_t e, uint32_t s) {  // (e 
 }
 
 // scratch layout per warp (uint16, [row][32 lanes]):
-//   rows [0, 2delta)        : log S_{i+1}
-//   rows [2delta, 4delta)   : log Omega_i
-//   rows [4delta, 4delta+k) : log Lambda_odd(alpha^-j), j < k
+//   rows [0, delta+1)                 : sentinel GF_LOG0 (log S_i for i <= 0)
+//   rows [delta+1, delta+1+2delta)    : log S_{i+1}
+//   rows [.., +2delta)                : log Omega_i
+//   rows [.., +k)                     : log Lambda_odd(alpha^-j), j < k
 template <class P> struct S3Scratch {
-  static constexpr uint32_t ROWS = 4 * P::DELTA + P::K;
+  static constexpr uint32_t PAD = P::DELTA + 1;
+  static constexpr uint32_t ROWS = PAD + 4 * P::DELTA + P::K;
   static constexpr uint32_t BYTES = ROWS * 32 * 2;
 };
 
@@ -46,48 +48,55 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   constexpr int TD = P::TWO_DELTA, DL = P::DELTA, N1 = P::N1, K = P::K;
   const uint8_t *EXPT = gf->exp;
   const uint16_t *LOGT = gf->log;
-  uint16_t *lS = scr;
-  uint16_t *lOm = scr + TD * 32;
-  uint16_t *lOdd = scr + 2 * TD * 32;
+  constexpr int PAD = S3Scratch<P>::PAD;
+#pragma unroll
+  for (int k = 0; k < PAD; k++) scr[k * 32 + lane] = GF_LOG0;
+  uint16_t *lS = scr + PAD * 32;  // lS[i*32 + lane] = log S_{i+1}; rows -PAD..-1 hold the sentinel
+  uint16_t *lOm = lS + TD * 32;
+  uint16_t *lOdd = lOm + TD * 32;
 
-  // ---- syndromes: S_i = sum_j sym_j alpha^{ij}
-  uint32_t S[TD];
+  // ---- syndromes: S_i = sum_j sym_j alpha^{ij}, in halves of at most 32 registers
+  constexpr int HALF = TD > 32 ? (TD + 1) / 2 : TD;
 #pragma unroll
-  for (int i = 0; i < TD; i++) S[i] = 0;
+  for (int i0 = 0; i0 < TD; i0 += HALF) {
+    uint32_t S[HALF];
+#pragma unroll
+    for (int i = 0; i < HALF; i++) S[i] = 0;
 #pragma unroll 1
-  for (int j = 0; j < N1; j++) {
-    const uint32_t x = sym_at(j);
-    const uint32_t zm = x ? 0xFFu : 0u;
-    uint32_t e = x ? LOGT[x] : 0u;  // e = log x + i*j (mod 255), i = 1..2delta
-    const uint32_t jj = (uint32_t)j % 255u;
+    for (int j = 0; j < N1; j++) {
+      const uint32_t x = sym_at(j);
+      const uint32_t zm = x ? 0xFFu : 0u;
+      const uint32_t jj = (uint32_t)j % 255u;
+      // e = log x + (i0 + 1 + i) * j (mod 255)
+      uint32_t e = x ? LOGT[x] : 0u;
+      e = (e + (uint32_t)i0 * jj) % 255u;
 #pragma unroll
-    for (int i = 0; i < TD; i++) {
-      e = mod255_add(e, jj);
-      S[i] ^= EXPT[e] & zm;
+      for (int i = 0; i < HALF; i++) {
+        e = mod255_add(e, jj);
+        if (i0 + i < TD) S[i] ^= EXPT[e] & zm;
+      }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < TD; i++) lS[i * 32 + lane] = LOGT[S[i]];
+    for (int i = 0; i < HALF; i++)
+      if (i0 + i < TD) lS[(i0 + i) * 32 + lane] = LOGT[S[i]];
+  }
 
   // ---- Berlekamp–Massey (Massey 1969) with Bx = x^m * B, logs of Bx kept
-  uint32_t Lam[DL + 1], lBx[DL + 1], win[DL + 1], lLam[DL + 1];
+  uint32_t Lam[DL + 1], lBx[DL + 1], lLam[DL + 1];
 #pragma unroll
   for (int k = 0; k <= DL; k++) {
     Lam[k] = (k == 0);
     lBx[k] = (k == 1) ? 0u : GF_LOG0;  // Bx = x * 1
-    win[k] = GF_LOG0;                    // win[k] = log S_{r+1-k} (sentinel for r - k < 0)
   }
   uint32_t L = 0, lb = 0;
 #pragma unroll 1
   for (int r = 0; r < TD; r++) {
-#pragma unroll
-    for (int k = DL; k >= 1; k--) win[k] = win[k - 1];
-    win[0] = lS[r * 32 + lane];
+    const uint16_t *wr = lS + r * 32 + lane;  // wr[-32k] = log S_{r+1-k} (sentinel for r < k)
     uint32_t d = 0;
 #pragma unroll
     for (int k = 0; k <= DL; k++) {
       lLam[k] = LOGT[Lam[k]];
-      d ^= EXPT[lLam[k] + win[k]];
+      d ^= EXPT[lLam[k] + wr[-32 * k]];
     }
     const uint32_t ld = LOGT[d];
     const uint32_t lc = d ? mod255_sub(ld, lb) : GF_LOG0;  // log(d / b)
@@ -108,21 +117,19 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   }
 
   // ---- Chien search over the n1 positions (+ Lambda_odd for the k message positions)
-  uint32_t ek[DL + 1], zk[DL + 1];
+  // ek = log Lambda_k - j*k (mod 255), or GF_LOG0 (never updated) for a zero coefficient
+  uint32_t ek[DL + 1];
 #pragma unroll
-  for (int k = 0; k <= DL; k++) {
-    zk[k] = Lam[k] ? 0xFFu : 0u;
-    ek[k] = Lam[k] ? lLam[k] : 0u;  // log Lambda_k - j*k (mod 255)
-  }
+  for (int k = 0; k <= DL; k++) ek[k] = lLam[k];
   uint32_t nroots = 0, rootmask = 0;
 #pragma unroll 1
   for (int j = 0; j < N1; j++) {
     uint32_t ev = 0, od = 0;
 #pragma unroll
     for (int k = 0; k <= DL; k++) {
-      const uint32_t t = EXPT[ek[k]] & zk[k];
+      const uint32_t t = EXPT[ek[k]];
       if (k & 1) od ^= t; else ev ^= t;
-      ek[k] = mod255_sub(ek[k], (uint32_t)k % 255u);
+      ek[k] = ek[k] == GF_LOG0 ? GF_LOG0 : mod255_sub(ek[k], (uint32_t)k % 255u);
     }
     const uint32_t root = (ev == od) ? 1u : 0u;
     nroots += root;
@@ -134,16 +141,12 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
 
   // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta
-#pragma unroll
-  for (int k = 0; k <= DL; k++) win[k] = GF_LOG0;
 #pragma unroll 1
   for (int i = 0; i < TD; i++) {
-#pragma unroll
-    for (int k = DL; k >= 1; k--) win[k] = win[k - 1];
-    win[0] = lS[i * 32 + lane];
+    const uint16_t *wi = lS + i * 32 + lane;
     uint32_t om = 0;
 #pragma unroll
-    for (int t = 0; t <= DL; t++) om ^= EXPT[lLam[t] + win[t]];
+    for (int t = 0; t <= DL; t++) om ^= EXPT[lLam[t] + wi[-32 * t]];
     lOm[i * 32 + lane] = LOGT[om];
   }
 

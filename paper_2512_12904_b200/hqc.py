@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
             "hqc_count_mismatch": [P, vp, vp, sz, vp, vp],
             "hqc_validate_support": [P, vp, sz, vp, vp],
             "hqc_decrypt_launch_shape": [P, sz, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+            "hqc_keygen_batch": [P, vp, vp, vp, vp, sz, vp],
+            "hqc_encrypt_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -173,3 +175,24 @@ def hqc_decrypt_launch_shape(level: int, batch: int) -> tuple[int, int]:
     g, w = ctypes.c_int(0), ctypes.c_int(0)
     _check(lib().hqc_decrypt_launch_shape(ctypes.byref(_cp(level)), batch, ctypes.byref(g), ctypes.byref(w)))
     return g.value, w.value
+
+
+def hqc_keygen_batch(level: int, h, x, y, s_out, stream=None) -> None:
+    """s = x + h*y per key (Alg. 3)."""
+    p = params(level)
+    K = _rows(h, 8 * p.u_stride, "h")
+    assert _rows(x, 4 * p.y_stride, "x") == K and _rows(y, 4 * p.y_stride, "y") == K
+    assert _rows(s_out, 8 * p.u_stride, "s_out") == K
+    _check(lib().hqc_keygen_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(x), _ptr(y), _ptr(s_out), K,
+                                  _stream(stream)))
+
+
+def hqc_encrypt_batch(level: int, h, s, key_index, m, r1, r2, e, u_out, v_out, stream=None) -> None:
+    """u = r1 + h*r2, v = trunc(mG + s*r2 + e) per ciphertext (Alg. 1); key_index may be None."""
+    p = params(level)
+    B = _rows(m, p.k, "m")
+    for t, nm in ((r1, "r1"), (r2, "r2"), (e, "e")):
+        assert _rows(t, 4 * p.e_stride, nm) == B
+    assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
+    _check(lib().hqc_encrypt_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(key_index), _ptr(m), _ptr(r1),
+                                   _ptr(r2), _ptr(e), _ptr(u_out), _ptr(v_out), B, _stream(stream)))

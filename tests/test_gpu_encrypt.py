@@ -1,0 +1,103 @@
+"""GPU KeyGen product and Encrypt against the oracle, bit-exact, on
+generator draws; plus the GPU encrypt -> GPU decrypt round trip at a full BASELINE size."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2512_12904_b200 import gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2512_12904_b200 import hqc  # noqa: E402
+from workloads import shape_for, valid_batch  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(DEV)
+
+
+def host(t, dtype, cols):
+    return t.cpu().numpy().view(dtype).reshape(-1, cols)
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_keygen_matches_oracle(level):
+    p = oracle.params(level)
+    g = hqc.params(level)
+    sh = shape_for(level)
+    h, x, y = gen.key_draws(0xABC, sh, 0, 9)
+    h[3, p.words - 1] |= np.uint64(0xFFFF) << np.uint64(p.n % 64)  # pad bits of h are ignored
+    ref = np.stack([oracle.keygen(p, h[i, : p.words] & _mask(p), x[i], y[i]) for i in range(9)])
+    s = torch.empty(9 * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_keygen_batch(level, dev(h), dev(x), dev(y), s)
+    torch.cuda.synchronize()
+    got = host(s, np.uint64, g.u_stride)
+    assert (got[:, : p.words] == ref).all()
+    assert (got[:, p.words:] == 0).all()
+
+
+def _mask(p):
+    m = np.full(p.words, np.uint64(0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+    m[-1] = np.uint64((1 << (p.n % 64)) - 1)
+    return m
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_encrypt_matches_oracle(level):
+    W = valid_batch(level, 20_000, 70)
+    p, g = W["params"], hqc.params(level)
+    B = 70
+    # pad the key rows to u_stride
+    H = np.zeros((W["h"].shape[0], g.u_stride), np.uint64)
+    H[:, : W["h"].shape[1]] = W["h"]
+    S = np.zeros_like(H)
+    S[:, : p.words] = W["s"]
+    key = W["key"].astype(np.uint32)
+    u = torch.empty(B * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    v = torch.empty(B * g.v_words * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_encrypt_batch(level, dev(H), dev(S), dev(key), dev(W["m"]), dev(W["r1"]), dev(W["r2"]), dev(W["e"]), u, v)
+    torch.cuda.synchronize()
+    gu = host(u, np.uint64, g.u_stride)
+    gv = host(v, np.uint64, g.v_words)
+    assert (gu == W["u"]).all()
+    assert (gv == W["v"]).all()
+
+
+@pytest.mark.parametrize("level,B", [(3, 65536)])
+def test_gpu_encrypt_decrypt_round_trip_full_size(level, B):
+    """configs[1] at full size entirely on the device: GPU keygen + encrypt of generator draws, then the
+    fused decrypt; every row must return its message (property at any size), and a sample of rows is
+    re-encrypted by the oracle to confirm the ciphertexts themselves."""
+    g = hqc.params(level)
+    sh = shape_for(level)
+    seed = 0x5151
+    nk = (B + 255) // 256
+    h, x, y = gen.key_draws(seed, sh, 0, nk)
+    m, r1, r2, e = gen.ct_draws(seed, sh, 0, B)
+    key = gen.key_of(0, B).astype(np.uint32)
+    s = torch.empty(nk * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    dh = dev(h)
+    hqc.hqc_keygen_batch(level, dh, dev(x), dev(y), s)
+    u = torch.empty(B * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    v = torch.empty(B * g.v_words * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_encrypt_batch(level, dh, s, dev(key), dev(m), dev(r1), dev(r2), dev(e), u, v)
+    yrows = dev(y[key])
+    mo = torch.empty(B * g.k, dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch(level, u, v, yrows, mo)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    hqc.hqc_count_mismatch(level, mo, dev(m), cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    p = oracle.params(level)
+    idx = np.random.default_rng(7).choice(B, 16, replace=False)
+    sh_np = host(s, np.uint64, g.u_stride)
+    gu, gv = host(u, np.uint64, g.u_stride), host(v, np.uint64, g.v_words)
+    for i in idx:
+        k = key[i]
+        ou, ov = oracle.encrypt(p, h[k], sh_np[k], m[i], r1[i], r2[i], e[i])
+        assert (gu[i, : p.words] == ou).all() and (gv[i] == ov).all()
