@@ -116,16 +116,14 @@ class ClockSampler:
 
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    from paper_2512_12904_b200 import dist as hdist
+
+    return hdist.env()
 
 
 def make_inputs(level: int, i0: int, B: int, p, nthreads=None):
-    """Seeded synthetic ciphertexts. v0: uniformly random u and v with the key's y
-    (config 4's fourth-quarter construction): the decrypt path is constant-flow, so its throughput
-    does not depend on whether the ciphertext decodes."""
+    """Uniformly random u and v with the key's y (config 4's fourth-quarter construction), host arrays
+    (--data random). The decrypt path is constant-flow: its speed does not depend on decodability."""
     from paper_2512_12904_b200 import gen
 
     seed = CONFIG_SEED[level]
@@ -138,61 +136,117 @@ def make_inputs(level: int, i0: int, B: int, p, nthreads=None):
     return u, v, y
 
 
-def cpu_baseline(level: int, u, v, y, got: np.ndarray | None, budget_s: float = 12.0) -> dict:
-    """The oracle, as it stands, on this host's cores over a bounded sample of the same inputs."""
+def gen_shape(p):
+    from paper_2512_12904_b200 import gen
+
+    return gen.Shape(n=p.n, w=p.w, wr=p.wr, n1=p.n1, k=p.k, n2=p.n2, delta=p.delta, u_stride=p.u_stride,
+                     v_words=p.v_words, y_stride=p.y_stride, sup_stride=p.e_stride)
+
+
+def make_valid_workload(level: int, i0: int, B: int, p, dev, chunk: int = 1 << 18):
+    """Valid ciphertexts for BASELINE configs[0..2] built on the device: the seeded
+    generator draws keys (h, x, y; one keypair per 256 ciphertexts) and per-ciphertext (m, r1, r2, e)
+    on the host; the library's keygen/encrypt kernels produce s, u, v.
+    Returns device tensors u, v, y (per-ciphertext rows) and m_ref."""
+    import torch
+
+    from paper_2512_12904_b200 import gen, hqc
+
+    seed = CONFIG_SEED[level]
+    sh = gen_shape(p)
+    key = gen.key_of(i0, B)
+    k0, nk = int(key[0]), int(key[-1] - key[0] + 1)
+    h, x, y = gen.key_draws(seed, sh, k0, nk)
+
+    def d(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(dev)
+
+    dh = d(h)
+    ds = torch.empty(nk * p.u_stride * 8, dtype=torch.uint8, device=dev)
+    hqc.hqc_keygen_batch(level, dh, d(x), d(y), ds)
+    du = torch.empty((B, p.u_stride * 8), dtype=torch.uint8, device=dev)
+    dv = torch.empty((B, p.v_words * 8), dtype=torch.uint8, device=dev)
+    dm = torch.empty((B, p.k), dtype=torch.uint8, device=dev)
+    for c0 in range(0, B, chunk):
+        n = min(chunk, B - c0)
+        m, r1, r2, e = gen.ct_draws(seed, sh, i0 + c0, n)
+        kidx = (key[c0:c0 + n] - k0).astype(np.uint32)
+        dmm = d(m)
+        hqc.hqc_encrypt_batch(level, dh, ds, d(kidx), dmm, d(r1), d(r2), d(e), du[c0:c0 + n], dv[c0:c0 + n])
+        dm[c0:c0 + n] = dmm.view(n, p.k)
+    dy = d(y[key - k0])
+    torch.cuda.synchronize(dev)
+    return du.view(-1), dv.view(-1), dy, dm.view(-1)
+
+
+def cpu_baseline(level: int, u, v, y, got, m_ref=None, budget_s: float = 12.0) -> dict:
+    """The oracle, as it stands, on this host's cores over a bounded sample of the same inputs; also
+    reports, on that sample, how many oracle outputs differ from the GPU's and from the messages."""
     import oracle
 
     op = oracle.params(level)
     cores = os.cpu_count() or 1
     done, t_total, n = 0, 0.0, max(cores, 64)
-    mism = 0
+    mism = mism_ref = 0
     while t_total < budget_s and done < u.shape[0]:
         n = min(n, u.shape[0] - done)
         sl = slice(done, done + n)
         t0 = time.perf_counter()
         m = oracle.decrypt_batch(op, u[sl], v[sl], y[sl], nthreads=cores)
         t_total += time.perf_counter() - t0
-        if got is not None:
-            mism += int((m != got[sl]).any(axis=1).sum())
+        mism += int((m != got[sl]).any(axis=1).sum())
+        if m_ref is not None:
+            mism_ref += int((m != m_ref[sl]).any(axis=1).sum())
         done += n
         n *= 2
     return {"value": done / t_total, "unit": "decryptions/s", "cores": cores, "kind": "oracle",
             "sample": f"first {done} ciphertexts of this rank's batch, oracle decrypt on {cores} threads "
-                      f"({t_total:.1f} s)", "parity_mismatches_vs_gpu": mism}
+                      f"({t_total:.1f} s)",
+            "parity_mismatches_vs_gpu": mism,
+            "oracle_vs_message_mismatches": mism_ref if m_ref is not None else None}
 
 
 def run_reference(args):
+    """This tier has no installable reference implementation (/root/reference holds only the paper):
+    the reference arm is the oracle, as it stands, on this host's cores, over a bounded sample of the
+    same workload (oracle-encrypted valid ciphertexts of the same generator draws)."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    from paper_2512_12904_b200 import gen  # noqa: F401  (input generator only)
     import oracle
 
+    from paper_2512_12904_b200 import gen
+
     op = oracle.params(args.level)
-
-    class P:  # the generator needs only sizes
-        n, w, n12 = op.n, op.w, op.n12
-        u_stride = op.words + (op.words & 1)
-        v_words = op.vwords
-        y_stride = (op.w + 3) // 4 * 4
-
     cores = os.cpu_count() or 1
     per_step = max(cores * 8, 64)
-    u, v, y = make_inputs(args.level, 0, per_step, P)
+    sh = gen.Shape(n=op.n, w=op.w, wr=op.wr, n1=op.n1, k=op.k, n2=op.n2, delta=op.delta,
+                   u_stride=op.words + (op.words & 1), v_words=op.vwords, y_stride=(op.w + 3) // 4 * 4,
+                   sup_stride=(op.wr + 3) // 4 * 4)
+    seed = CONFIG_SEED[args.level]
+    key = gen.key_of(0, per_step)
+    nk = int(key[-1]) + 1
+    h, x, y = gen.key_draws(seed, sh, 0, nk)
+    s = np.stack([oracle.keygen(op, h[i, : op.words], x[i], y[i]) for i in range(nk)])
+    m, r1, r2, e = gen.ct_draws(seed, sh, 0, per_step)
+    u, v = oracle.encrypt_batch(op, h, s, key, m, r1, r2, e, nthreads=cores)
+    yy = np.ascontiguousarray(y[key])
     for _ in range(args.warmup):
-        oracle.decrypt_batch(op, u[:cores], v[:cores], y[:cores], nthreads=cores)
+        oracle.decrypt_batch(op, u[:cores], v[:cores], yy[:cores], nthreads=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.decrypt_batch(op, u, v, y, nthreads=cores)
+        got = oracle.decrypt_batch(op, u, v, yy, nthreads=cores)
     dt = time.perf_counter() - t0
     val = per_step * args.steps / dt
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "decryptions/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32 (GF(2), GF(2^8))",
-           "data": "synthetic", "config": {"workload": WORKLOAD[args.level] + " (bounded CPU sample)",
-                                           "level": args.level, "batch_per_step": per_step},
+           "data": "synthetic: seeded valid ciphertexts (generator draws, oracle keygen+encrypt)",
+           "config": {"workload": WORKLOAD[args.level] + " (bounded CPU sample)", "level": args.level,
+                      "batch_per_step": per_step},
+           "mismatches_vs_message": int((got != m).any(axis=1).sum()),
            "cpu_baseline": {"value": val, "unit": "decryptions/s", "cores": cores, "kind": "oracle",
-                            "sample": f"{per_step} ciphertexts per step"},
+                            "sample": f"{per_step} ciphertexts per step, {args.steps} steps"},
            "e2e": {"value": val, "unit": "decryptions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -200,11 +254,12 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--level", type=int, default=3, choices=[1, 3, 5])
     ap.add_argument("--batch", type=int, default=65536, help="ciphertexts per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--data", default="valid", choices=["valid", "random"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -214,6 +269,7 @@ def main():
     import torch
     import torch.distributed as dist
 
+    from paper_2512_12904_b200 import dist as hdist
     from paper_2512_12904_b200 import hqc
 
     world, rank, local = dist_setup()
@@ -223,14 +279,16 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     p = hqc.params(args.level)
     B = args.batch
-    i0 = rank * B
-    u, v, y = make_inputs(args.level, i0, B, p)
-    du = torch.from_numpy(u.view(np.uint8)).to(dev)
-    dv = torch.from_numpy(v.view(np.uint8)).to(dev)
-    dy = torch.from_numpy(y.view(np.uint8)).to(dev)
+    i0, B = hdist.shard(rank, B)  # this rank's shard of the seeded workload (weak scaling)
+    if args.data == "valid":
+        du, dv, dy, dref = make_valid_workload(args.level, i0, B, p, dev)
+    else:
+        du, dv, dy = (torch.from_numpy(a.view(np.uint8)).to(dev) for a in make_inputs(args.level, i0, B, p))
+        dref = None
     dm = torch.empty(B * p.k, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    # ---- timed region: K fused-kernel launches between CUDA events on the launching stream
     for _ in range(args.warmup):
         hqc.hqc_decrypt_batch(args.level, du, dv, dy, dm)
     torch.cuda.synchronize()
@@ -244,18 +302,25 @@ def main():
             hqc.hqc_decrypt_batch(args.level, du, dv, dy, dm)
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        dist.barrier()
+    ms = hdist.max_over_ranks(ev0.elapsed_time(ev1), dev)
     value = world * B * args.steps / (ms / 1e3)
 
-    # ---- e2e: host (pinned) buffers through the same C-ABI call, copies inside the timed region
-    hu, hv, hy = (torch.from_numpy(a.view(np.uint8)).pin_memory() for a in (u, v, y))
+    # ---- correctness of the timed outputs: mismatches vs the generator's messages, summed over ranks
+    mismatches = None
+    if dref is not None:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        hqc.hqc_count_mismatch(args.level, dm, dref, cnt)
+        mismatches = hdist.sum_over_ranks(cnt)
+
+    # ---- e2e: pinned host buffers through the same C-ABI call, H2D of u,v,y and D2H of m timed
+    hu, hv, hy = (t.cpu().pin_memory() for t in (du, dv, dy))
     hm = torch.empty(B * p.k, dtype=torch.uint8).pin_memory()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0.record(stream)
     for _ in range(args.e2e_steps):
         du.copy_(hu, non_blocking=True)
@@ -265,45 +330,48 @@ def main():
         hm.copy_(dm, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ems], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
+    ems = hdist.max_over_ranks(e0.elapsed_time(e1), dev)
     e2e = {"value": world * B * args.e2e_steps / (ems / 1e3), "unit": "decryptions/s",
-           "h2d_bytes_per_step": int(u.nbytes + v.nbytes + y.nbytes), "d2h_bytes_per_step": int(B * p.k)}
+           "h2d_bytes_per_step": int(hu.numel() + hv.numel() + hy.numel()), "d2h_bytes_per_step": int(B * p.k)}
 
-    got = dm.cpu().numpy().reshape(B, p.k)
     ops = algorithmic_ops(p)
     peaks = measured_peaks()
     c = clk.summary()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     kernel_s = ms / 1e3 / args.steps
-    achieved_tops = ops["total"] * B / kernel_s / 1e12
-    peak_tops = 64 * sms * sm_max * 1e6 / 1e12  # ALU pipe: 64 lanes/clk/SM
-    roof = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Tintop/s",
-            "frac": achieved_tops / peak_tops, "traffic": None,
+    achieved = ops["total"] * B / kernel_s / 1e12
+    peak = 64 * sms * sm_max * 1e6 / 1e12  # ALU pipe: 64 lanes/clk/SM (K7-measured 63.7)
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tintop/s", "frac": achieved / peak,
+            "traffic": None,
             "peak_source": f"64 ALU lanes/clk/SM x {sms} SMs x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "ops_per_decryption": ops["total"],
-            "frac_at_measured_clock": (achieved_tops / (64 * sms * c["sm_mhz"] * 1e6 / 1e12)) if c["sm_mhz"] else None,
+            "frac_at_measured_clock": (achieved / (64 * sms * c["sm_mhz"] * 1e6 / 1e12)) if c["sm_mhz"] else None,
+            "roofline_decryptions_per_s": peak * 1e12 / ops["total"],
             "hbm_gbs": ops["abi_bytes"] * B / kernel_s / 1e9,
             "hbm_frac": ops["abi_bytes"] * B / kernel_s / 1e9 / float(peaks.get("hbm_gbs", 6538.6)),
-            "roofline_decryptions_per_s": peak_tops * 1e12 / ops["total"]}
+            "smem_bound_decryptions_per_s": 32 * sms * sm_max * 1e6 / ops["pairs"]}
     gw = hqc.hqc_decrypt_launch_shape(args.level, B)
     out = {"metric": METRIC, "value": value, "unit": "decryptions/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u8/u32 (GF(2), GF(2^8))",
-           "data": "synthetic: uniformly random u,v + seeded key supports (constant-flow path)",
+           "data": ("synthetic: seeded valid ciphertexts (generator draws, GPU keygen+encrypt)" if dref is not None
+                    else "synthetic: uniformly random u,v + seeded key supports (constant-flow path)"),
+           "mismatches_vs_message": mismatches,
            "config": {"workload": WORKLOAD[args.level], "level": args.level, "batch_per_gpu": B,
                       "global_batch": world * B, "parallelism": f"dp{world}",
-                      "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB > 126 MB L2, no flush needed",
-                      "launch": {"grid": gw[0], "warps_per_cta": gw[1]}},
+                      "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB/GPU > 126 MB L2, no flush needed",
+                      "launch": {"kernel": "k_decrypt (fused)", "grid": gw[0], "warps_per_cta": gw[1]}},
            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
            "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"],
                       "samples": c["samples"], "source": "NVML, 2 ms period, timed region only"}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.level, u, v, y, got)
+        got = hm.numpy().reshape(B, p.k)
+        u = hu.numpy().view(np.uint64).reshape(B, -1)
+        v = hv.numpy().view(np.uint64).reshape(B, -1)
+        y = hy.numpy().view(np.uint32).reshape(B, -1)
+        m_ref = dref.cpu().numpy().reshape(B, p.k) if dref is not None else None
+        out["cpu_baseline"] = cpu_baseline(args.level, u, v, y, got, m_ref)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
