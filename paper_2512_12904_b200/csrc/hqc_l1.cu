@@ -1,0 +1,25 @@
+// Level-1 instantiation of the kernels (own translation unit: own constant bank).
+#include "kernels.cuh"
+#include "launchers.h"
+
+namespace hqc {
+using PL = Lv<1>;
+int decrypt_l1(const uint64_t *u, const uint64_t *v, const uint32_t *y, uint8_t *m, size_t batch, cudaStream_t st) {
+  return launch_decrypt<PL>(u, v, y, m, batch, st);
+}
+int stage1_l1(const uint64_t *u, const uint32_t *y, const uint64_t *v, uint64_t *r, size_t batch, cudaStream_t st) {
+  return launch_stage1<PL>(u, y, v, r, batch, st);
+}
+int stage2_l1(const uint64_t *r, uint8_t *sym, size_t batch, cudaStream_t st) { return launch_stage2<PL>(r, sym, batch, st); }
+int stage3_l1(const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t batch, cudaStream_t st) {
+  return launch_stage3<PL>(sym, m, ok, batch, st);
+}
+int keygen_l1(const uint64_t *h, const uint32_t *x, const uint32_t *y, uint64_t *s, size_t nkeys, cudaStream_t st) {
+  return launch_keygen<PL>(h, x, y, s, nkeys, st);
+}
+int encrypt_l1(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m, const uint32_t *r1,
+                const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v, size_t batch, cudaStream_t st) {
+  return launch_encrypt<PL>(h, s, key, m, r1, r2, e, u, v, batch, st);
+}
+int shape_l1(size_t batch, int *grid, int *wpc) { return shape_impl<PL>(batch, grid, wpc); }
+}  // namespace hqc
