@@ -20,6 +20,15 @@ def nvcc_cmd(out: str, extra: list[str] | None = None) -> list[str]:
             "-shared", "-o", out, *[os.path.join(CSRC, s) for s in SOURCES], *(extra or [])]
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """Experiment builds (scripts/exp_variants.py) into a separate .so; never used by the product."""
+    r = subprocess.run(nvcc_cmd(out, [f"-D{d}" for d in defines]), capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed")
+    return out
+
+
 def up_to_date() -> bool:
     if not os.path.exists(SO):
         return False

@@ -12,26 +12,13 @@
 #pragma once
 #include <cstdint>
 
+#include "gf256.cuh"
 #include "levels.cuh"
 #include "stage1.cuh"
 
 namespace hqc {
 
-// ---- compile-time RS generator tables -------------------------------------------------------------
-constexpr uint32_t gf_mul_c(uint32_t a, uint32_t b) {  // carry-less product mod 0x11D (compile time)
-  uint32_t r = 0;
-  for (int i = 0; i < 8; i++)
-    if ((b >> i) & 1) r ^= a << i;
-  for (int d = 14; d >= 8; d--)
-    if ((r >> d) & 1) r ^= 0x11Du << (d - 8);
-  return r;
-}
-constexpr uint32_t gf_pow_c(uint32_t a, uint32_t e) {
-  uint32_t r = 1;
-  for (uint32_t i = 0; i < e; i++) r = gf_mul_c(r, a);
-  return r;
-}
-
+// ---- compile-time RS generator tables (gf_mul_c / gf_exp_c from gf256.cuh)
 template <uint32_t TD> struct RsEncTable {
   uint8_t t[256][TD];  // t[f][j] = g*_j * f
 };
@@ -40,7 +27,7 @@ template <uint32_t TD> constexpr RsEncTable<TD> make_rs_enc_table() {
   uint32_t g[TD + 1] = {};
   g[0] = 1;
   for (uint32_t i = 1; i <= TD; i++) {
-    const uint32_t root = gf_pow_c(2, 255 - i);
+    const uint32_t root = gf_exp_c(255 - i);
     for (uint32_t t = i; t > 0; t--) g[t] = g[t - 1] ^ gf_mul_c(g[t], root);
     g[0] = gf_mul_c(g[0], root);
   }

@@ -34,6 +34,21 @@ constexpr GfTables make_gf_tables() {
 
 __device__ __constant__ GfTables c_gf = make_gf_tables();
 
+// compile-time GF(2^8) arithmetic for building the constant tables below and in encrypt.cuh
+constexpr uint32_t gf_mul_c(uint32_t a, uint32_t b) {  // carry-less product mod 0x11D
+  uint32_t r = 0;
+  for (int i = 0; i < 8; i++)
+    if ((b >> i) & 1) r ^= a << i;
+  for (int d = 14; d >= 8; d--)
+    if ((r >> d) & 1) r ^= 0x11Du << (d - 8);
+  return r;
+}
+constexpr uint32_t gf_exp_c(uint32_t e) {  // alpha^e, alpha = 0x02
+  uint32_t r = 1;
+  for (uint32_t i = 0; i < e % 255; i++) r = gf_mul_c(r, 2);
+  return r;
+}
+
 // Copy the tables into a CTA's shared memory (all threads of the CTA participate).
 __device__ __forceinline__ void gf_tables_to_smem(GfTables *dst) {
   const uint32_t *src = reinterpret_cast<const uint32_t *>(&c_gf);

@@ -1,4 +1,5 @@
 // Level-1 instantiation of the kernels (own translation unit: own constant bank).
+#define HQC_THIS_LEVEL 1
 #include "kernels.cuh"
 #include "launchers.h"
 

@@ -85,13 +85,13 @@ template <class P> struct S1Pipe {
     uint32_t acc[S::R];
     s1_product<P, S>(E, dsm, acc, lane);
     __syncwarp();  // every lane is done reading E: r overwrites it
-    s1_store_r<S>(acc, E, lane);
-    __syncwarp();
     if (v) {
-      wait();
-      s1_xor_v<P::NW>(E, stg_u, lane);
-      __syncwarp();
+      wait();  // v has landed in the staging buffer during the product loop
+      s1_store_r_xor<S>(acc, E, stg_u, lane);
+    } else {
+      s1_store_r<S>(acc, E, lane);
     }
+    __syncwarp();
     if (has_next) issue_uy(next, lane);
   }
 };
@@ -165,50 +165,108 @@ __global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym,
   }
 }
 
-// K4: fused decrypt. Persistent warps; warp g owns ciphertexts [g*per, (g+1)*per) and walks them in
-// chunks of 32: stage 1 (whole warp) and stage 2 (lane per RM block) per ciphertext, symbols parked
-// in shared memory as [j][slot]; then stage 3 with one lane per ciphertext of the chunk.
+// K4: fused decrypt, one warp PAIR (one 64-thread CTA) per ciphertext at a time. The pair shares the
+// ciphertext's doubled-u copy E: both warps build it, each warp runs the rotate-and-XOR over half of
+// the support indices, warp 1 hands its accumulators to warp 0 through shared memory, warp 0 adds v
+// and writes r. Stage 2 spreads the n1 RM blocks over the 64 threads; stage 3 decodes a chunk of 64
+// ciphertexts, one per thread. Rows of the next ciphertext are fetched by TMA during stage 2/3.
+// Sharing E halves the shared memory per warp (more resident warps to hide latency) and lets the two
+// warps finish a ciphertext's stage 2 in one round for n1 <= 64.
+template <class P> struct PairSmem {
+  using S = DecShape<P>;
+  static constexpr uint32_t XOFF = round_up(P::NW, 4);  // warp-1 accumulator image, above r in E
+  static_assert(XOFF + P::NW <= S::E_WORDS, "the accumulator image fits in E above r");
+  static constexpr uint32_t E_BYTES = round_up(
+      S::E_WORDS * 4 > 2 * S3Scratch<P>::BYTES ? S::E_WORDS * 4 : 2 * S3Scratch<P>::BYTES, 16);
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
+  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 64, 16);
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16;
+  static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // warp 0 takes indices [0, W0), warp 1 [W0, W)
+};
+
 template <class P>
-__global__ void __launch_bounds__(128) k_decrypt(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
-                                                 const uint32_t *__restrict__ y, uint8_t *__restrict__ m_out,
-                                                 size_t batch, size_t per) {
+__global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
+                                                const uint32_t *__restrict__ y, uint8_t *__restrict__ m_out,
+                                                size_t batch, size_t per) {
+  using S = DecShape<P>;
+  using M = PairSmem<P>;
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  uint8_t *base_p = smem + GF_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(base_p);
+  uint32_t *stg_u = reinterpret_cast<uint32_t *>(base_p + M::E_BYTES);
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(base_p + M::E_BYTES + M::STG_UV_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(base_p + M::E_BYTES + M::STG_BYTES);
+  uint8_t *sym = base_p + M::E_BYTES + M::STG_BYTES + M::D_BYTES;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sym + M::SYM_BYTES);
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   gf_tables_to_smem(gf);
+  if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t *ws = smem + GF_BYTES + (size_t)wib * WarpSmem<P>::BYTES;
-  S1Pipe<P> pipe(ws, u, v, y, lane);
-  uint8_t *sb = ws + WarpSmem<P>::S1_BYTES;
-  const size_t g = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  const size_t lo = g * per;
+  uint32_t phase = 0;
+  auto issue_uy = [&](size_t ct) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, M::UB + M::YB);
+    tma_load_1d(stg_u, u + ct * P::U_STRIDE, M::UB, bar);
+    tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar);
+  };
+  const size_t lo = (size_t)blockIdx.x * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
-  if (lo < hi) pipe.issue_uy(lo, lane);
-  for (size_t base = lo; base < hi; base += 32) {
-    const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
+  if (lo < hi && tid == 0) issue_uy(lo);
+  const uint32_t j0 = wid ? M::W0 : 0u, j1 = wid ? P::W : M::W0;
+  for (size_t base = lo; base < hi; base += 64) {
+    const uint32_t rows = (uint32_t)(hi - base < 64 ? hi - base : 64);
     for (uint32_t s = 0; s < rows; s++) {
       const size_t ct = base + s;
-      pipe.run(ct, ct + 1 < hi, ct + 1, lane);
-      for (uint32_t j = lane; j < P::N1; j += 32) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
+      mbar_wait(bar, phase);  // u, y of ct
+      phase ^= 1u;
+      s1_stage_d<P, S, 64>(stg_y, dsm, tid);
+      s1_build_E<P, S, 64>(stg_u, E, tid);
+      __syncthreads();
+      if (tid == 0) {  // v lands in the staging buffer while the product runs
+        fence_proxy_async_smem();
+        mbar_expect_tx(bar, M::VB);
+        tma_load_1d(stg_u, v + ct * P::V_WORDS, M::VB, bar);
+      }
+      uint32_t acc[S::R];
+      s1_product_range<P, S>(E, dsm, acc, lane, j0, j1);
+      __syncthreads();  // both warps are done reading E
+      if (wid == 1) s1_store_r<S>(acc, E + M::XOFF, lane);
+      __syncthreads();
+      mbar_wait(bar, phase);  // v of ct
+      phase ^= 1u;
+      if (wid == 0) s1_store_r_xor2<S>(acc, E, E + M::XOFF, stg_u, lane);
+      __syncthreads();
+      if (tid == 0 && ct + 1 < hi) issue_uy(ct + 1);
+#ifndef HQC_EXP_SKIP
+#define HQC_EXP_SKIP 0  // experiments only (scripts/exp_variants.py): 1 = skip stage 2, 2 = skip stage 3
+#endif
+      if (!(HQC_EXP_SKIP & 1))
+      for (uint32_t j = tid; j < P::N1; j += 64) {  // stage 2: one RM block per thread
+        const uint4 *src = reinterpret_cast<const uint4 *>(E) + j * (P::N2 / 128);
         uint32_t X[P::MULT * 4];
 #pragma unroll
         for (int c = 0; c < (int)P::MULT; c++) {
           const uint4 x = src[c];
           X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
         }
-        sb[j * 32 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+        sym[j * 64 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
       }
-      __syncwarp();
+      __syncthreads();
     }
-    for (uint32_t s = rows; s < 32; s++)
-      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * 32 + s] = 0;
-    __syncwarp();
-    const bool act = (uint32_t)lane < rows;
-    auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
-    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
-                      act ? m_out + (base + lane) * P::K : nullptr);
-    __syncwarp();
+    for (uint32_t e = tid; e < P::N1 * 64; e += 64)
+      if ((e & 63) >= rows) sym[e] = 0;
+    __syncthreads();
+    const uint32_t slot = 32 * wid + lane;
+    const bool act = slot < rows;
+    auto sym_at = [&](int j) -> uint32_t { return sym[j * 64 + slot]; };
+    if (!(HQC_EXP_SKIP & 2))
+      rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(base_p + wid * S3Scratch<P>::BYTES), lane,
+                        act ? m_out + (base + slot) * P::K : nullptr);
+    __syncthreads();
   }
 }
 
@@ -224,9 +282,10 @@ struct DevInfo {
 static std::mutex g_mu;
 static DevInfo g_dev[16];
 
-constexpr int WARPS_PER_CTA = 1;  // fused / stage-1 kernels: one warp per CTA (fine-grained SM balance)
+constexpr int WARPS_PER_CTA = 1;  // stage-1 kernel: one warp per CTA (fine-grained SM balance)
+constexpr int DEC_THREADS = 64;   // fused kernel: one warp pair per CTA
 
-template <class P> static uint32_t decrypt_smem() { return GF_BYTES + WARPS_PER_CTA * WarpSmem<P>::BYTES; }
+template <class P> static uint32_t decrypt_smem() { return GF_BYTES + PairSmem<P>::BYTES; }
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
@@ -241,7 +300,7 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaFuncSetAttribute(k_stage1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_stage3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage3_smem<P>(4))) != cudaSuccess) return e;
   int c = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt<P>, 32 * WARPS_PER_CTA, decrypt_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt<P>, DEC_THREADS, decrypt_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt[P::level] = c > 0 ? c : 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
@@ -256,17 +315,16 @@ static int cur_device(DevInfo **out) {
   return dev;
 }
 
-// Work split of the fused kernel: every resident warp gets an equal contiguous range (at least
-// MIN_PER ciphertexts, so the lane-per-ciphertext RS stage keeps most lanes busy).
-constexpr size_t MIN_PER = 16;
+// Work split of the fused kernel: every resident CTA (warp pair) gets an equal contiguous range of at
+// least MIN_PER ciphertexts (the lane-per-ciphertext RS stage wants full chunks).
+constexpr size_t MIN_PER = 32;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
-  const size_t cap = (size_t)di.sms * di.cap_decrypt[P::level] * WARPS_PER_CTA;
-  size_t warps = (batch + MIN_PER - 1) / MIN_PER;
-  if (warps > cap) warps = cap;
-  if (warps == 0) warps = 1;
-  *per = (batch + warps - 1) / warps;
-  const size_t used = (batch + *per - 1) / *per;
-  *grid = (int)((used + WARPS_PER_CTA - 1) / WARPS_PER_CTA);
+  const size_t cap = (size_t)di.sms * di.cap_decrypt[P::level];
+  size_t ctas = (batch + MIN_PER - 1) / MIN_PER;
+  if (ctas > cap) ctas = cap;
+  if (ctas == 0) ctas = 1;
+  *per = (batch + ctas - 1) / ctas;
+  *grid = (int)((batch + *per - 1) / *per);
 }
 
 template <class P>
@@ -278,7 +336,7 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
   int grid;
   size_t per;
   decrypt_shape<P>(*di, batch, &grid, &per);
-  k_decrypt<P><<<grid, 32 * WARPS_PER_CTA, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
+  k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
@@ -350,7 +408,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
-  *wpc = WARPS_PER_CTA;
+  *wpc = DEC_THREADS / 32;
   return HQC_OK;
 }
 

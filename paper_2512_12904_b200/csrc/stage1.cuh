@@ -20,21 +20,21 @@
 namespace hqc {
 
 // Build E (S::E_WORDS words) from the staged dense row su (shared memory).
-template <class P, class S>
+template <class P, class S, int NT = 32>
 __device__ __forceinline__ void s1_build_E(const uint32_t *su, uint32_t *E, int lane) {
   constexpr uint32_t NV = P::Q0 / 4;
   constexpr uint32_t MASK_C = (1u << P::C) - 1u;
   // words below Q0: u itself
-  for (uint32_t c = lane; c < NV; c += 32)
+  for (uint32_t c = lane; c < NV; c += NT)
     reinterpret_cast<uint4 *>(E)[c] = reinterpret_cast<const uint4 *>(su)[c];
-  for (uint32_t q = 4 * NV + lane; q < P::Q0; q += 32) E[q] = su[q];
+  for (uint32_t q = 4 * NV + lane; q < P::Q0; q += NT) E[q] = su[q];
   const uint32_t eq0 = su[P::Q0] & MASK_C;  // the last C bits of u; bits >= n are ignored (R#13)
   // word Q0: the last C bits of u, then u continues from bit 0 (the wrap of X^n = 1)
   if (lane == 0) E[P::Q0] = eq0 | (su[0] << P::C);
   // words above Q0: E word q holds u bits [32q - n, 32q - n + 32) = funnel(u32[x], u32[x+1], 32 - C)
   // with x = q - Q0 - 1. Words that no valid output reads are filled with zeros.
 #pragma unroll 4
-  for (uint32_t q = P::Q0 + 1 + lane; q < S::E_WORDS; q += 32) {
+  for (uint32_t q = P::Q0 + 1 + lane; q < S::E_WORDS; q += NT) {
     const uint32_t x = q - P::Q0 - 1;
     const uint32_t lo = x < P::Q0 ? su[x] : (x == P::Q0 ? eq0 : 0u);
     const uint32_t hi = x + 1 < P::Q0 ? su[x + 1] : (x + 1 == P::Q0 ? eq0 : 0u);
@@ -43,24 +43,26 @@ __device__ __forceinline__ void s1_build_E(const uint32_t *su, uint32_t *E, int 
 }
 
 // The WT rotation amounts d_j = n - y_j from the staged support row (an entry >= n is treated as 0).
-template <class P, class S>
+template <class P, class S, int NT = 32>
 __device__ __forceinline__ void s1_stage_d(const uint32_t *sy, uint32_t *dsm, int lane) {
-  for (uint32_t j = lane; j < S::WPAD; j += 32) {
+  for (uint32_t j = lane; j < S::WPAD; j += NT) {
     const uint32_t y = sy[j];
     dsm[j] = (j < S::WT && y < P::N) ? P::N - y : P::N;
   }
 }
 
-// The WT-iteration rotate-and-XOR. acc[k] accumulates output word lane*R + k.
+// The rotate-and-XOR over support indices [j0, j1) (j0 even; the loop count is fixed by the level,
+// not by the data). acc[k] accumulates output word lane*R + k.
 template <class P, class S>
-__device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
-                                           int lane) {
+__device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
+                                                 int lane, uint32_t j0, uint32_t j1) {
   constexpr int R = S::R;
 #pragma unroll
   for (int k = 0; k < R; k++) acc[k] = 0;
   const uint32_t *Eb = E + lane * R;
+  uint32_t j = j0;
 #pragma unroll 1
-  for (uint32_t j = 0; j + 1 < S::WT; j += 2) {  // two indices per pass: one 3-input XOR per word
+  for (; j + 1 < j1; j += 2) {  // two indices per pass: one 3-input XOR per word
     const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
     const uint32_t *p0 = Eb + (dd.x >> 5);
     const uint32_t *p1 = Eb + (dd.y >> 5);
@@ -73,8 +75,8 @@ __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *ds
       b0 = b1;
     }
   }
-  if (S::WT & 1) {
-    const uint32_t d = dsm[S::WT - 1];
+  if (j < j1) {
+    const uint32_t d = dsm[j];
     const uint32_t *p0 = Eb + (d >> 5);
     uint32_t a0 = p0[0];
 #pragma unroll
@@ -86,12 +88,36 @@ __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *ds
   }
 }
 
+template <class P, class S>
+__device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
+                                           int lane) {
+  s1_product_range<P, S>(E, dsm, acc, lane, 0, S::WT);
+}
+
 // Store the accumulators (S::NOUT words, aliasing E). The caller synchronises the warp first.
 template <class S>
 __device__ __forceinline__ void s1_store_r(const uint32_t (&acc)[S::R], uint32_t *rsm, int lane) {
 #pragma unroll
   for (int k = 0; k < (int)S::R; k++)
     if (lane * S::R + k < S::NOUT) rsm[lane * S::R + k] = acc[k];
+}
+
+// Store acc XOR v (v staged in shared memory): lane L reads v words L*R + k — R odd, conflict-free.
+template <class S>
+__device__ __forceinline__ void s1_store_r_xor(const uint32_t (&acc)[S::R], uint32_t *rsm, const uint32_t *sv,
+                                               int lane) {
+#pragma unroll
+  for (int k = 0; k < (int)S::R; k++)
+    if (lane * S::R + k < S::NOUT) rsm[lane * S::R + k] = acc[k] ^ sv[lane * S::R + k];
+}
+
+// Store acc XOR x XOR v, where x is another warp's accumulator image (same word layout).
+template <class S>
+__device__ __forceinline__ void s1_store_r_xor2(const uint32_t (&acc)[S::R], uint32_t *rsm, const uint32_t *xs,
+                                                const uint32_t *sv, int lane) {
+#pragma unroll
+  for (int k = 0; k < (int)S::R; k++)
+    if (lane * S::R + k < S::NOUT) rsm[lane * S::R + k] = acc[k] ^ xs[lane * S::R + k] ^ sv[lane * S::R + k];
 }
 
 // r ^= v with v staged in shared memory (16-byte chunks).

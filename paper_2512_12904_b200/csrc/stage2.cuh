@@ -4,15 +4,14 @@
 // The oracle defines F(a) = sum_p s_p (-1)^{a.p} with s_p = mult - 2*cnt_p (cnt_p = number of copies
 // with bit p set) and picks the smallest a with maximal |F(a)|, sign -> bit 7. Here:
 //   1. bit-sliced copy counting: cnt_p in 2 (mult 3) or 3 (mult 5) bit planes, 32 positions per op;
-//   2. cnt as exact fp16 in half2 registers: register i = 16q + l holds positions (32q+l, 32q+l+16);
-//      the value is built with the 1024-magic (0x6400 | cnt is the half 1024 + cnt);
+//   2. soft values -2*cnt as exact fp16 in half2 registers: register i = 16q + l holds positions
+//      (32q+l, 32q+l+16), built per bit plane with fp16 fma tricks (mostly FMA-pipe work);
 //   3. the 128-point fast Walsh–Hadamard transform: 6 butterfly stages across registers (HADD2 on
 //      the FMA pipe) and one in-register stage (HFMA2 with a (1,-1) multiplier). Every value is an
 //      integer of magnitude <= 640 < 2048, so fp16 arithmetic is exact;
-//   4. G(a) = F'(a) for a != 0, G(0) = F'(0) - 64*mult, where F' is the transform of cnt; then
-//      F = -2G, so argmax |F| = argmax |G| and F(a*) < 0 <=> G(a*) > 0;
-//   5. M = max |G| (HMNMX2 tree), then 128-bit masks of {|G| = M} and {G = M} in natural a order;
-//      a* = lowest set bit (smallest a, R#11), bit 7 = [G(a*) = M].
+//   4. F = FWHT(-2 cnt) + 128*mult*[a = 0]: exactly the oracle's F;
+//   5. M = max |F| (HMNMX2 tree), then 128-bit masks of {|F| = M} and {F = -M} in natural a order;
+//      a* = lowest set bit (smallest a, R#11), bit 7 = [F(a*) = -M].
 #pragma once
 #include <cuda_fp16.h>
 
@@ -21,6 +20,14 @@
 namespace hqc {
 
 __device__ __forceinline__ __half2 u2h(uint32_t x) { return *reinterpret_cast<__half2 *>(&x); }
+
+// (a & m) | c as ONE lop3 (keeps the compiler from re-deriving a per use); m and c in registers
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t m, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(m), "r"(c));
+  return d;
+}
+
 
 // X[c*4 + q] = 32-bit word q of copy c of the block.
 template <int MULT>
@@ -44,15 +51,36 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
     }
   }
 
+  // soft values v_p = -2*cnt_p (the constant mult of s_p = mult - 2 cnt_p is added to F(0) below), built
+  // per bit plane k as y_k = -2^{k+1} b_k in exact fp16 arithmetic (1 LOP3 + 1 HFMA2 per plane):
+  //   l <= 9 : x = (plane & bits{l, l+16}) | 0x6400 -> the halves are 1024 + 2^l b (mantissa bit l);
+  //            y_k = fma(x, -2^{k+1-l}, 2^{k+11-l});
+  //   10 <= l <= 14: the same on plane >> 5 (one shift per plane word) with l - 5;
+  //   l = 15 : bits 15, 31 are the fp16 sign bits: h = (plane & 0x80008000) | 1.0 = +-1 = 1 - 2b,
+  //            y_k = fma(h, 2^k, -2^k).
   __half2 h[64];
-  const __half2 k1024 = __float2half2_rn(1024.0f);
 #pragma unroll
   for (int q = 0; q < 4; q++) {
+    uint32_t pls[NPL];
+#pragma unroll
+    for (int k = 0; k < NPL; k++) pls[k] = pl[k][q] >> 5;
 #pragma unroll
     for (int l = 0; l < 16; l++) {
-      uint32_t t = 0x64006400u | ((pl[0][q] >> l) & 0x00010001u) | (((pl[1][q] >> l) & 0x00010001u) << 1);
-      if constexpr (NPL == 3) t |= ((pl[2][q] >> l) & 0x00010001u) << 2;
-      h[16 * q + l] = __hsub2(u2h(t), k1024);
+      __half2 acc;
+#pragma unroll
+      for (int k = 0; k < NPL; k++) {
+        __half2 y;
+        if (l < 15) {
+          const int lb = l <= 9 ? l : l - 5;
+          const uint32_t x = and_or(l <= 9 ? pl[k][q] : pls[k], 0x00010001u << lb, 0x64006400u);
+          y = __hfma2(u2h(x), __float2half2_rn(-ldexpf(1.0f, k + 1 - lb)), __float2half2_rn(ldexpf(1.0f, k + 11 - lb)));
+        } else {
+          const uint32_t hx = and_or(pl[k][q], 0x80008000u, 0x3C003C00u);
+          y = __hfma2(u2h(hx), __float2half2_rn(ldexpf(1.0f, k)), __float2half2_rn(-ldexpf(1.0f, k)));
+        }
+        acc = (k == 0) ? y : __hadd2(acc, y);
+      }
+      h[16 * q + l] = acc;
     }
   }
 
@@ -71,10 +99,10 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
   const __half2 pm = __halves2half2(__float2half(1.0f), __float2half(-1.0f));
 #pragma unroll
   for (int i = 0; i < 64; i++) h[i] = __hfma2(__high2half2(h[i]), pm, __low2half2(h[i]));
-  // a = 0 correction: G(0) = F'(0) - 64*mult
-  h[0] = __hsub2(h[0], __halves2half2(__float2half(64.0f * MULT), __float2half(0.0f)));
+  // a = 0: F(0) += 128 * mult (the constant part of the soft values)
+  h[0] = __hadd2(h[0], __halves2half2(__float2half(128.0f * MULT), __float2half(0.0f)));
 
-  // M = max |G| (balanced tree for ILP)
+  // M = max |F| (balanced tree for ILP)
   __half2 m[32];
 #pragma unroll
   for (int i = 0; i < 32; i++) m[i] = __hmax2(__habs2(h[i]), __habs2(h[i + 32]));
@@ -84,6 +112,7 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
     for (int i = 0; i < s; i++) m[i] = __hmax2(m[i], m[i + s]);
   const __half Mh = __hmax(__low2half(m[0]), __high2half(m[0]));
   const __half2 M2 = __half2half2(Mh);
+  const __half2 nM2 = __hneg2(M2);
 
   // masks in natural order: word q = i >> 4 holds a in [32q, 32q+32); bit (i&15) + 16*half
   uint32_t absw[4] = {0u, 0u, 0u, 0u}, posw[4] = {0u, 0u, 0u, 0u};
@@ -91,7 +120,7 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
   for (int i = 0; i < 64; i++) {
     const uint32_t bit = 0x00010001u << (i & 15);
     absw[i >> 4] |= __heq2_mask(__habs2(h[i]), M2) & bit;
-    posw[i >> 4] |= __heq2_mask(h[i], M2) & bit;
+    posw[i >> 4] |= __heq2_mask(h[i], nM2) & bit;  // F(a) = -M: the codeword's bit 7 is set
   }
   // smallest a with |G(a)| = M (lowest set bit, lowest word first)
   uint32_t a = 0, pw = 0;

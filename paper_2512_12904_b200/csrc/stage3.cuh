@@ -30,15 +30,63 @@ __device__ __forceinline__ uint32_t mod255_add(uint32_t e, uint32_t s) {  // (e 
 }
 
 // scratch layout per warp (uint16, [row][32 lanes]):
-//   rows [0, delta+1)                 : sentinel GF_LOG0 (log S_i for i <= 0)
-//   rows [delta+1, delta+1+2delta)    : log S_{i+1}
-//   rows [.., +2delta)                : log Omega_i
-//   rows [.., +k)                     : log Lambda_odd(alpha^-j), j < k
+//   rows [0, delta+1)              : sentinel GF_LOG0 (log S_i for i <= 0)
+//   rows [delta+1, delta+1+2delta) : log S_{i+1}; overwritten in place by log Omega_i
+//   rows [.., +k)                  : Lambda_t (linear Chien input, t <= delta < k), then log Lambda_odd(alpha^-j)
 template <class P> struct S3Scratch {
   static constexpr uint32_t PAD = P::DELTA + 1;
-  static constexpr uint32_t ROWS = PAD + 4 * P::DELTA + P::K;
+  static constexpr uint32_t ROWS = PAD + 2 * P::DELTA + P::K;
   static constexpr uint32_t BYTES = ROWS * 32 * 2;
+  static_assert(P::K >= P::DELTA + 1, "Lambda rows alias the Lambda_odd rows");
 };
+
+// ---- GF(2)-linear maps as constant tables -------------------------------------------------------
+// The syndromes are a GF(2)-linear function of the received bits: S = XOR over (j, b) with bit b of
+// sym_j set of SYN[j][b], where SYN[j][b] packs alpha^{(i+1) j} * 2^b for i < 2delta (4 per word).
+// Likewise the Chien values Lambda(alpha^-j), j < n1, and Lambda_odd(alpha^-j), j < k, are linear in
+// the bits of Lambda: XOR over (t, b) with bit b of Lambda_t set of CHN[t][b] (bytes j < n1: the
+// contribution 2^b alpha^{-jt}; bytes n1 + j, j < k: the same for odd t, else 0). Every lane of a warp
+// reads the same table word at the same time, so the tables live in the constant bank (uniform
+// LDCU loads, no shared-memory traffic and no bank conflicts) — one table set per level per
+// translation unit (hqc_lN.cu). A table set larger than the bank budget falls back to log/antilog.
+template <class P> struct RsLinear {
+  static constexpr uint32_t SW = (P::TWO_DELTA + 3) / 4;        // syndrome words
+  static constexpr uint32_t CW = (P::N1 + P::K + 3) / 4;        // Chien-vector words
+  static constexpr uint32_t SYN_BYTES = P::N1 * 8 * SW * 4;
+  static constexpr uint32_t CHN_BYTES = (P::DELTA + 1) * 8 * CW * 4;
+  static constexpr bool LINEAR_CHIEN = SYN_BYTES + CHN_BYTES + sizeof(GfTables) <= 60 * 1024;
+  static constexpr uint32_t CHN_T = LINEAR_CHIEN ? P::DELTA + 1 : 1;
+  struct Tables {
+    uint32_t syn[P::N1][8][SW];
+    uint32_t chn[CHN_T][8][CW];
+  };
+  static constexpr Tables make() {
+    uint32_t ex[255] = {};
+    uint32_t x = 1;
+    for (int e = 0; e < 255; e++) {
+      ex[e] = x;
+      x = gf_mul_c(x, 2);
+    }
+    Tables T{};
+    for (uint32_t j = 0; j < P::N1; j++)
+      for (uint32_t b = 0; b < 8; b++)
+        for (uint32_t i = 0; i < P::TWO_DELTA; i++)
+          T.syn[j][b][i / 4] |= gf_mul_c(1u << b, ex[((i + 1) * j) % 255]) << (8 * (i % 4));
+    if (LINEAR_CHIEN)
+      for (uint32_t t = 0; t < CHN_T; t++)
+        for (uint32_t b = 0; b < 8; b++)
+          for (uint32_t j = 0; j < P::N1; j++) {
+            const uint32_t v = gf_mul_c(1u << b, ex[(255 - (j * t) % 255) % 255]);
+            T.chn[t][b][j / 4] |= v << (8 * (j % 4));
+            if (j < P::K && (t & 1)) T.chn[t][b][(P::N1 + j) / 4] |= v << (8 * ((P::N1 + j) % 4));
+          }
+    return T;
+  }
+};
+
+#ifdef HQC_THIS_LEVEL
+__device__ __constant__ RsLinear<Lv<HQC_THIS_LEVEL>>::Tables c_rs_lin = RsLinear<Lv<HQC_THIS_LEVEL>>::make();
+#endif
 
 // sym_at(j) returns the j-th received symbol of this lane's ciphertext.
 // Writes K message bytes to out[0..K) (out may be null for inactive lanes). Returns ok.
@@ -52,33 +100,28 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
 #pragma unroll
   for (int k = 0; k < PAD; k++) scr[k * 32 + lane] = GF_LOG0;
   uint16_t *lS = scr + PAD * 32;  // lS[i*32 + lane] = log S_{i+1}; rows -PAD..-1 hold the sentinel
-  uint16_t *lOm = lS + TD * 32;
-  uint16_t *lOdd = lOm + TD * 32;
+  uint16_t *lOm = lS;  // Omega overwrites the syndromes in place (computed from the top down)
+  uint16_t *lOdd = lS + TD * 32;
+  uint16_t *sLam = lOdd;  // read completely before lOdd is written
+  using LIN = RsLinear<P>;
 
-  // ---- syndromes: S_i = sum_j sym_j alpha^{ij}, in halves of at most 32 registers
-  constexpr int HALF = TD > 32 ? (TD + 1) / 2 : TD;
+  // ---- syndromes S_i = sum_j sym_j alpha^{ij} (i = 1..2delta) as the GF(2)-linear map SYN
+  {
+    uint32_t Sw[LIN::SW];
 #pragma unroll
-  for (int i0 = 0; i0 < TD; i0 += HALF) {
-    uint32_t S[HALF];
-#pragma unroll
-    for (int i = 0; i < HALF; i++) S[i] = 0;
+    for (int w = 0; w < (int)LIN::SW; w++) Sw[w] = 0;
 #pragma unroll 1
     for (int j = 0; j < N1; j++) {
       const uint32_t x = sym_at(j);
-      const uint32_t zm = x ? 0xFFu : 0u;
-      const uint32_t jj = (uint32_t)j % 255u;
-      // e = log x + (i0 + 1 + i) * j (mod 255)
-      uint32_t e = x ? LOGT[x] : 0u;
-      e = (e + (uint32_t)i0 * jj) % 255u;
 #pragma unroll
-      for (int i = 0; i < HALF; i++) {
-        e = mod255_add(e, jj);
-        if (i0 + i < TD) S[i] ^= EXPT[e] & zm;
+      for (int b = 0; b < 8; b++) {
+        const uint32_t m = 0u - ((x >> b) & 1u);
+#pragma unroll
+        for (int w = 0; w < (int)LIN::SW; w++) Sw[w] ^= c_rs_lin.syn[j][b][w] & m;
       }
     }
 #pragma unroll
-    for (int i = 0; i < HALF; i++)
-      if (i0 + i < TD) lS[(i0 + i) * 32 + lane] = LOGT[S[i]];
+    for (int i = 0; i < TD; i++) lS[i * 32 + lane] = LOGT[(Sw[i / 4] >> (8 * (i % 4))) & 0xFFu];
   }
 
   // ---- Berlekamp–Massey (Massey 1969) with Bx = x^m * B, logs of Bx kept
@@ -117,32 +160,64 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   }
 
   // ---- Chien search over the n1 positions (+ Lambda_odd for the k message positions)
-  // ek = log Lambda_k - j*k (mod 255), or GF_LOG0 (never updated) for a zero coefficient
-  uint32_t ek[DL + 1];
-#pragma unroll
-  for (int k = 0; k <= DL; k++) ek[k] = lLam[k];
   uint32_t nroots = 0, rootmask = 0;
-#pragma unroll 1
-  for (int j = 0; j < N1; j++) {
-    uint32_t ev = 0, od = 0;
+  if constexpr (LIN::LINEAR_CHIEN) {
 #pragma unroll
-    for (int k = 0; k <= DL; k++) {
-      const uint32_t t = EXPT[ek[k]];
-      if (k & 1) od ^= t; else ev ^= t;
-      ek[k] = ek[k] == GF_LOG0 ? GF_LOG0 : mod255_sub(ek[k], (uint32_t)k % 255u);
+    for (int t = 0; t <= DL; t++) sLam[t * 32 + lane] = (uint16_t)Lam[t];
+    uint32_t Cw[LIN::CW];
+#pragma unroll
+    for (int w = 0; w < (int)LIN::CW; w++) Cw[w] = 0;
+#pragma unroll 1
+    for (int t = 0; t <= DL; t++) {
+      const uint32_t x = sLam[t * 32 + lane];
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        const uint32_t m = 0u - ((x >> b) & 1u);
+#pragma unroll
+        for (int w = 0; w < (int)LIN::CW; w++) Cw[w] ^= c_rs_lin.chn[t][b][w] & m;
+      }
     }
-    const uint32_t root = (ev == od) ? 1u : 0u;
-    nroots += root;
-    if (j < K) {
-      rootmask |= root << j;
-      lOdd[j * 32 + lane] = LOGT[od];
+#pragma unroll
+    for (int w = 0; w < (int)((N1 + 3) / 4); w++) {
+      // bit 7 of each byte of nz is set iff that byte of Cw[w] is nonzero (no carries between bytes)
+      const uint32_t nz = (((Cw[w] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | Cw[w]) & 0x80808080u;
+      uint32_t zero = ~nz & 0x80808080u;
+      if (4 * w + 4 > N1) zero &= 0x80808080u >> (8 * (4 * w + 4 - N1));  // only positions j < n1
+      nroots += __popc(zero);
+#pragma unroll
+      for (int c = 0; c < 4; c++)
+        if (4 * w + c < K) rootmask |= ((zero >> (8 * c + 7)) & 1u) << (4 * w + c);
+    }
+#pragma unroll
+    for (int j = 0; j < K; j++) lOdd[j * 32 + lane] = LOGT[(Cw[(N1 + j) / 4] >> (8 * ((N1 + j) % 4))) & 0xFFu];
+  } else {
+    // ek = log Lambda_k - j*k (mod 255), or GF_LOG0 (never updated) for a zero coefficient
+    uint32_t ek[DL + 1];
+#pragma unroll
+    for (int k = 0; k <= DL; k++) ek[k] = lLam[k];
+#pragma unroll 1
+    for (int j = 0; j < N1; j++) {
+      uint32_t ev = 0, od = 0;
+#pragma unroll
+      for (int k = 0; k <= DL; k++) {
+        const uint32_t t = EXPT[ek[k]];
+        if (k & 1) od ^= t; else ev ^= t;
+        ek[k] = ek[k] == GF_LOG0 ? GF_LOG0 : mod255_sub(ek[k], (uint32_t)k % 255u);
+      }
+      const uint32_t root = (ev == od) ? 1u : 0u;
+      nroots += root;
+      if (j < K) {
+        rootmask |= root << j;
+        lOdd[j * 32 + lane] = LOGT[od];
+      }
     }
   }
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
 
-  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta
+  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta, from i = 2delta-1 down:
+  //      Omega_i reads log S_{i'+1} for i' <= i only, so it may overwrite row i in place
 #pragma unroll 1
-  for (int i = 0; i < TD; i++) {
+  for (int i = TD - 1; i >= 0; i--) {
     const uint16_t *wi = lS + i * 32 + lane;
     uint32_t om = 0;
 #pragma unroll

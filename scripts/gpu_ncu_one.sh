@@ -1,0 +1,8 @@
+# one ncu --set full capture of the fused kernel at level $L (default 3)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+L=${L:-3}
+CMD="python scripts/prof_kernels.py --level $L --only fused --iters 2"
+timeout 300 $CMD > gpurun_out/prof_plain_L$L.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_decrypt -s 3 -c 1 -o gpurun_out/prof_fused_L$L $CMD > gpurun_out/ncu_fused_L$L.log 2>&1
+echo "exit $?"
