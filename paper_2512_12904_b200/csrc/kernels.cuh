@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/hqc_gpu.h"
 #include "async_copy.cuh"
@@ -165,6 +167,61 @@ __global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym,
   }
 }
 
+#ifndef HQC_DEC_MINCTAS  // min resident CTAs (register cap) of the pair kernel, swept in scripts/exp_occ.py
+#define HQC_DEC_MINCTAS (P::level == 5 ? 6 : (P::level == 1 ? 14 : 8))
+#endif
+#ifndef HQC_DEC_MINCTAS_W1
+#define HQC_DEC_MINCTAS_W1 (P::level == 5 ? 12 : 20)
+#endif
+
+// K4a: fused decrypt, one warp per ciphertext (the pair-free variant). Warp g owns ciphertexts
+// [g*per, (g+1)*per) in chunks of 32: stage 1 + stage 2 per ciphertext (symbols parked as [j][slot]),
+// then stage 3 with one lane per ciphertext of the chunk. Chosen per level by DecPolicy below.
+template <class P>
+__global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uint64_t *__restrict__ u,
+                                                                     const uint64_t *__restrict__ v,
+                                                                     const uint32_t *__restrict__ y,
+                                                                     uint8_t *__restrict__ m_out, size_t batch,
+                                                                     size_t per) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint8_t *ws = smem + GF_BYTES;
+  S1Pipe<P> pipe(ws, u, v, y, lane);
+  uint8_t *sb = ws + WarpSmem<P>::S1_BYTES;
+  const size_t lo = (size_t)blockIdx.x * per;
+  const size_t hi = lo + per < batch ? lo + per : batch;
+  if (lo < hi) pipe.issue_uy(lo, lane);
+  for (size_t base = lo; base < hi; base += 32) {
+    const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
+    for (uint32_t s = 0; s < rows; s++) {
+      const size_t ct = base + s;
+      pipe.run(ct, ct + 1 < hi, ct + 1, lane);
+      for (uint32_t j = lane; j < P::N1; j += 32) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
+        uint32_t X[P::MULT * 4];
+#pragma unroll
+        for (int c = 0; c < (int)P::MULT; c++) {
+          const uint4 x = src[c];
+          X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+        }
+        sb[j * 32 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+      }
+      __syncwarp();
+    }
+    for (uint32_t s = rows; s < 32; s++)
+      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * 32 + s] = 0;
+    __syncwarp();
+    const bool act = (uint32_t)lane < rows;
+    auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
+    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
+                      act ? m_out + (base + lane) * P::K : nullptr);
+    __syncwarp();
+  }
+}
+
 // K4: fused decrypt, one warp PAIR (one 64-thread CTA) per ciphertext at a time. The pair shares the
 // ciphertext's doubled-u copy E: both warps build it, each warp runs the rotate-and-XOR over half of
 // the support indices, warp 1 hands its accumulators to warp 0 through shared memory, warp 0 adds v
@@ -173,26 +230,67 @@ __global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym,
 // Sharing E halves the shared memory per warp (more resident warps to hide latency) and lets the two
 // warps finish a ciphertext's stage 2 in one round for n1 <= 64.
 template <class P> struct PairSmem {
-  using S = DecShape<P>;
+  // Work split of stage 1 between the two warps:
+  //   SPLIT_WORDS: warp w computes output words [w*NW/2, (w+1)*NW/2) over all w indices (R = odd
+  //     ceil(NW/64)); no hand-off. Fewer registers and wasted lanes for HQC-1/5, but measured 3% and
+  //     1% slower than the index split on B200 (profiles/r01/NOTES.md), so it is off.
+  //   else: warp w takes half of the support indices over all NW words (R = odd ceil(NW/32); exact
+  //     35 for HQC-3), and warp 1 hands its accumulators to warp 0 through shared memory.
+  static constexpr bool SPLIT_WORDS = false;
+  static constexpr uint32_t NWH = P::NW / 2;
+  using S = typename std::conditional<SPLIT_WORDS, ProdShape<P, P::NW / 2, P::W>, DecShape<P>>::type;
+  static constexpr uint32_t EW_NEED = SPLIT_WORDS ? round_up(P::Q0 + NWH + 32 * S::R + 2, 4) : S::E_WORDS;
   static constexpr uint32_t XOFF = round_up(P::NW, 4);  // warp-1 accumulator image, above r in E
-  static_assert(XOFF + P::NW <= S::E_WORDS, "the accumulator image fits in E above r");
+  static_assert(SPLIT_WORDS || XOFF + P::NW <= S::E_WORDS, "the accumulator image fits in E above r");
+  static constexpr uint32_t E_WORDS = EW_NEED;
   static constexpr uint32_t E_BYTES = round_up(
-      S::E_WORDS * 4 > 2 * S3Scratch<P>::BYTES ? S::E_WORDS * 4 : 2 * S3Scratch<P>::BYTES, 16);
+      E_WORDS * 4 > 2 * S3Scratch<P>::BYTES ? E_WORDS * 4 : 2 * S3Scratch<P>::BYTES, 16);
   static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
   static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
-  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16);
+  // DSTAGE: a second staging buffer so the next ciphertext's u, y are fetched during this one's
+  // product loop (HQC-1: stage 2 alone is too short to hide the fetch; HQC-3/5 have no smem to spare
+  // and hide it already — profiles/r01/NOTES.md).
+  static constexpr bool DSTAGE = P::level == 1;
+  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16) + (DSTAGE ? STG_UV_BYTES : 0);
   static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
   static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 64, 16);
-  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16;
-  static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // warp 0 takes indices [0, W0), warp 1 [W0, W)
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16 * 2;
+  static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // index split: warp 0 takes [0, W0), warp 1 [W0, W)
+};
+
+// E built up to E_WORDS words (an E-build shape with the pair's E size)
+template <class P, uint32_t EW> struct EBuildShape {
+  static constexpr uint32_t E_WORDS = EW;
+};
+
+#ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (scripts/exp_variants.py)
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_T0() long long _t = clock64()
+#define PHASE(i) do { long long _n = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _t)); _t = _n; } while (0)
+#define HQC_CAT2(a, b) a##b
+#define HQC_CAT(a, b) HQC_CAT2(a, b)
+extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *host8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host8, g_phase_cycles, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -5;
+}
+#else
+#define PHASE_T0()
+#define PHASE(i)
+#endif
+// Register cap per level (minimum resident CTAs): the fused kernel is latency-bound at the occupancy
+// its register count allows, so the cap trades a few registers for more resident warp pairs.
+template <class P> struct DecOcc {
+  static constexpr int MIN_CTAS = HQC_DEC_MINCTAS;
 };
 
 template <class P>
-__global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
+__global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
                                                 const uint32_t *__restrict__ y, uint8_t *__restrict__ m_out,
                                                 size_t batch, size_t per) {
-  using S = DecShape<P>;
   using M = PairSmem<P>;
+  using S = typename M::S;
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);
   uint8_t *base_p = smem + GF_BYTES;
@@ -201,12 +299,17 @@ __global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, 
   uint32_t *stg_y = reinterpret_cast<uint32_t *>(base_p + M::E_BYTES + M::STG_UV_BYTES);
   uint32_t *dsm = reinterpret_cast<uint32_t *>(base_p + M::E_BYTES + M::STG_BYTES);
   uint8_t *sym = base_p + M::E_BYTES + M::STG_BYTES + M::D_BYTES;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sym + M::SYM_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sym + M::SYM_BYTES);  // u, y (and v unless DSTAGE)
+  uint32_t *stg_v = M::DSTAGE ? stg_y + round_up(M::YB, 16) / 4 : stg_u;
+  uint64_t *barv = M::DSTAGE ? bar + 1 : bar;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   gf_tables_to_smem(gf);
-  if (tid == 0) mbar_init(bar, 1);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    if (M::DSTAGE) mbar_init(barv, 1);
+  }
   __syncthreads();
-  uint32_t phase = 0;
+  uint32_t phase = 0, phasev = 0;
   auto issue_uy = [&](size_t ct) {
     fence_proxy_async_smem();
     mbar_expect_tx(bar, M::UB + M::YB);
@@ -221,26 +324,52 @@ __global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, 
     const uint32_t rows = (uint32_t)(hi - base < 64 ? hi - base : 64);
     for (uint32_t s = 0; s < rows; s++) {
       const size_t ct = base + s;
+      PHASE_T0();
       mbar_wait(bar, phase);  // u, y of ct
       phase ^= 1u;
+      PHASE(0);
       s1_stage_d<P, S, 64>(stg_y, dsm, tid);
-      s1_build_E<P, S, 64>(stg_u, E, tid);
+      s1_build_E<P, EBuildShape<P, M::E_WORDS>, 64>(stg_u, E, tid);
       __syncthreads();
       if (tid == 0) {  // v lands in the staging buffer while the product runs
         fence_proxy_async_smem();
-        mbar_expect_tx(bar, M::VB);
-        tma_load_1d(stg_u, v + ct * P::V_WORDS, M::VB, bar);
+        mbar_expect_tx(barv, M::VB);
+        tma_load_1d(stg_v, v + ct * P::V_WORDS, M::VB, barv);
+        if (M::DSTAGE && ct + 1 < hi) issue_uy(ct + 1);
       }
+      PHASE(1);
       uint32_t acc[S::R];
-      s1_product_range<P, S>(E, dsm, acc, lane, j0, j1);
-      __syncthreads();  // both warps are done reading E
-      if (wid == 1) s1_store_r<S>(acc, E + M::XOFF, lane);
+      if constexpr (M::SPLIT_WORDS) {
+        const uint32_t w0 = wid * M::NWH;  // this warp's first output word
+        s1_product_range<P, S>(E + w0, dsm, acc, lane, 0, P::W);
+        __syncthreads();  // both warps are done reading E
+        if (M::DSTAGE) {
+          mbar_wait(barv, phasev);  // v of ct
+          phasev ^= 1u;
+        } else {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        s1_store_r_xor<S>(acc, E + w0, stg_v + w0, lane);
+      } else {
+        s1_product_range<P, S>(E, dsm, acc, lane, j0, j1);
+        PHASE(2);
+        __syncthreads();  // both warps are done reading E
+        PHASE(3);
+        if (wid == 1) s1_store_r<S>(acc, E + M::XOFF, lane);
+        __syncthreads();
+        if (M::DSTAGE) {
+          mbar_wait(barv, phasev);  // v of ct
+          phasev ^= 1u;
+        } else {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        if (wid == 0) s1_store_r_xor2<S>(acc, E, E + M::XOFF, stg_v, lane);
+      }
       __syncthreads();
-      mbar_wait(bar, phase);  // v of ct
-      phase ^= 1u;
-      if (wid == 0) s1_store_r_xor2<S>(acc, E, E + M::XOFF, stg_u, lane);
-      __syncthreads();
-      if (tid == 0 && ct + 1 < hi) issue_uy(ct + 1);
+      PHASE(4);
+      if (!M::DSTAGE && tid == 0 && ct + 1 < hi) issue_uy(ct + 1);
 #ifndef HQC_EXP_SKIP
 #define HQC_EXP_SKIP 0  // experiments only (scripts/exp_variants.py): 1 = skip stage 2, 2 = skip stage 3
 #endif
@@ -255,7 +384,9 @@ __global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, 
         }
         sym[j * 64 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
       }
+      PHASE(5);
       __syncthreads();
+      PHASE(6);
     }
     for (uint32_t e = tid; e < P::N1 * 64; e += 64)
       if ((e & 63) >= rows) sym[e] = 0;
@@ -263,9 +394,11 @@ __global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, 
     const uint32_t slot = 32 * wid + lane;
     const bool act = slot < rows;
     auto sym_at = [&](int j) -> uint32_t { return sym[j * 64 + slot]; };
+    PHASE_T0();
     if (!(HQC_EXP_SKIP & 2))
       rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(base_p + wid * S3Scratch<P>::BYTES), lane,
                         act ? m_out + (base + slot) * P::K : nullptr);
+    PHASE(7);
     __syncthreads();
   }
 }
@@ -274,7 +407,8 @@ __global__ void __launch_bounds__(64) k_decrypt(const uint64_t *__restrict__ u, 
 // host side
 struct DevInfo {
   int sms = 0;
-  int cap_decrypt[6] = {0};  // resident CTAs/SM of k_decrypt per level
+  int cap_decrypt[6] = {0};     // resident CTAs/SM of k_decrypt per level
+  int cap_decrypt_w1[6] = {0};  // resident CTAs/SM of k_decrypt_w1 per level
   int cap_stage1[6] = {0};
   bool ready[6] = {false};
 };
@@ -286,6 +420,19 @@ constexpr int WARPS_PER_CTA = 1;  // stage-1 kernel: one warp per CTA (fine-grai
 constexpr int DEC_THREADS = 64;   // fused kernel: one warp pair per CTA
 
 template <class P> static uint32_t decrypt_smem() { return GF_BYTES + PairSmem<P>::BYTES; }
+template <class P> static uint32_t decrypt_w1_smem() { return GF_BYTES + WarpSmem<P>::BYTES; }
+
+// Which fused kernel a level uses (measured, profiles/r01/NOTES.md); HQC_DEC_KERNEL=1|2 overrides
+// (experiments only).
+template <class P> static bool use_pair() {
+  static int env = [] {
+    const char *s = getenv("HQC_DEC_KERNEL");
+    return s ? atoi(s) : 0;
+  }();
+  if (env == 1) return false;
+  if (env == 2) return true;
+  return P::level != 5;
+}
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
@@ -302,6 +449,9 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   int c = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt<P>, DEC_THREADS, decrypt_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt[P::level] = c > 0 ? c : 1;
+  if ((e = cudaFuncSetAttribute(k_decrypt_w1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_w1_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_w1<P>, 32, decrypt_w1_smem<P>())) != cudaSuccess) return e;
+  di.cap_decrypt_w1[P::level] = c > 0 ? c : 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   di.ready[P::level] = true;
@@ -319,8 +469,10 @@ static int cur_device(DevInfo **out) {
 // least MIN_PER ciphertexts (the lane-per-ciphertext RS stage wants full chunks).
 constexpr size_t MIN_PER = 32;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
-  const size_t cap = (size_t)di.sms * di.cap_decrypt[P::level];
-  size_t ctas = (batch + MIN_PER - 1) / MIN_PER;
+  const bool pair = use_pair<P>();
+  const size_t cap = (size_t)di.sms * (pair ? di.cap_decrypt[P::level] : di.cap_decrypt_w1[P::level]);
+  const size_t min_per = pair ? MIN_PER : MIN_PER / 2;
+  size_t ctas = (batch + min_per - 1) / min_per;
   if (ctas > cap) ctas = cap;
   if (ctas == 0) ctas = 1;
   *per = (batch + ctas - 1) / ctas;
@@ -336,7 +488,10 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
   int grid;
   size_t per;
   decrypt_shape<P>(*di, batch, &grid, &per);
-  k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
+  if (use_pair<P>())
+    k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
+  else
+    k_decrypt_w1<P><<<grid, 32, decrypt_w1_smem<P>(), st>>>(u, v, y, m, batch, per);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
@@ -408,7 +563,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
-  *wpc = DEC_THREADS / 32;
+  *wpc = use_pair<P>() ? DEC_THREADS / 32 : 1;
   return HQC_OK;
 }
 

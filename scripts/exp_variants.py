@@ -8,12 +8,46 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VAR = {"full": 0, "no_s2": 1, "no_s3": 2, "no_s2s3": 3}
+PHASES = ["wait_uy", "stage_d+buildE+sync", "product", "sync_after_product", "combine+wait_v+store",
+          "stage2", "sync_after_stage2", "stage3"]
 
 
 def build():
     from paper_2512_12904_b200 import build as b
     for name, skip in VAR.items():
         b.build_variant(os.path.join(ROOT, "scripts", f"libhqc_exp_{name}.so"), [f"HQC_EXP_SKIP={skip}"])
+    b.build_variant(os.path.join(ROOT, "scripts", "libhqc_exp_timing.so"), ["HQC_EXP_TIMING=1"])
+
+
+def timing():
+    """Per-phase warp-cycle totals of the fused kernel (lane 0 of each warp, clock64)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from bench import make_inputs
+    from paper_2512_12904_b200 import hqc
+
+    hqc.LIB_PATH = os.path.join(ROOT, "scripts", "libhqc_exp_timing.so")
+    L = hqc.lib()
+    out = {}
+    for level in (1, 3, 5):
+        p = hqc.params(level)
+        B = 65536
+        u, v, y = make_inputs(level, 0, B, p)
+        du, dv, dy = (torch.from_numpy(a.view(np.uint8)).cuda() for a in (u, v, y))
+        dm = torch.empty(B * p.k, dtype=torch.uint8, device="cuda")
+        f = getattr(L, f"hqc_exp_phases_l{level}")
+        buf = (ctypes.c_ulonglong * 8)()
+        hqc.hqc_decrypt_batch(level, du, dv, dy, dm)
+        f(buf)
+        hqc.hqc_decrypt_batch(level, du, dv, dy, dm)
+        f(buf)
+        tot = sum(buf)
+        out[level] = {PHASES[i]: round(100.0 * buf[i] / tot, 1) for i in range(8)}
+        out[level]["total_warp_cycles_per_ct"] = round(tot / B, 0)
+    print(json.dumps(out))
 
 
 def run():
@@ -48,4 +82,4 @@ def run():
 
 
 if __name__ == "__main__":
-    build() if sys.argv[1:] == ["build"] else run()
+    {"build": build, "timing": timing, "run": run}[sys.argv[1]]()

@@ -241,3 +241,36 @@ def test_full_size_adversarial():
     order = np.concatenate([np.tile(np.arange(k * q, (k + 1) * q), B // D) for k in range(4)])
     got = gpu_decrypt(1, dict(u=W["u"][order], v=W["v"][order], y=W["y"][order]))
     assert (got == ref[order]).all()
+
+
+# ---------------------------------------------------------------- both fused-kernel variants
+@pytest.mark.parametrize("kernel", ["1", "2"])
+def test_both_fused_kernel_variants(kernel, tmp_path):
+    """The library picks the warp-pair kernel (HQC-1/3) or the one-warp kernel (HQC-5) per level;
+    HQC_DEC_KERNEL forces either (read once per process), so each runs in a subprocess on every level."""
+    import subprocess
+    import sys
+    import os
+
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, "tests")
+import oracle
+from paper_2512_12904_b200 import hqc
+from workloads import valid_batch, adversarial_batch
+for level in (1, 3, 5):
+    W = valid_batch(level, 40000, 77) if level != 1 else adversarial_batch(0, 128, 128)
+    p = hqc.params(level)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
+    B = W["u"].shape[0]
+    m = torch.empty(B * p.k, dtype=torch.uint8, device="cuda")
+    hqc.hqc_decrypt_batch(level, d(W["u"]), d(W["v"]), d(W["y"]), m)
+    torch.cuda.synchronize()
+    ref = oracle.decrypt_batch(W["params"], W["u"], W["v"], W["y"])
+    assert (m.cpu().numpy().reshape(B, p.k) == ref).all(), level
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HQC_DEC_KERNEL=kernel)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
