@@ -135,6 +135,20 @@ int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
                       const uint32_t *r2, const uint32_t *e, uint64_t *u_out, uint64_t *v_out,
                       size_t batch, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Host-buffer decrypt (the end-to-end call): u_h, v_h, y_h, m_h are HOST arrays in the layouts of
+ * hqc_decrypt_batch (page-locked memory recommended; pageable memory works but copies synchronously).
+ * The batch is processed in chunks of `chunk` ciphertexts (0 = 8192) on two internal streams so that
+ * the H2D copy of chunk i+1, the fused kernel on chunk i and the D2H copy of chunk i-1 overlap.
+ * d_work: caller-owned DEVICE workspace of at least hqc_decrypt_host_workspace_bytes(p, chunk)
+ * bytes (else HQC_ERR_SIZE). Asynchronous with respect to the host: the work is ordered after prior
+ * work on `stream` and later work on `stream` waits for it; m_h is valid after synchronising `stream`.
+ * ------------------------------------------------------------------------------------------- */
+size_t hqc_decrypt_host_workspace_bytes(const hqc_params *p, size_t chunk);
+int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, const uint64_t *v_h,
+                           const uint32_t *y_h, uint8_t *m_h, size_t batch, void *d_work,
+                           size_t work_bytes, size_t chunk, void *stream);
+
 /* Number of persistent CTAs / warps the fused kernel launches for `batch` on the current device
  * (introspection for the bench's launch accounting). Returns HQC_OK. */
 int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);

@@ -192,3 +192,87 @@ extern "C" int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const u
   if (key_index && misaligned(key_index)) return HQC_ERR_ALIGN;
   HQC_DISPATCH(p, encrypt, h, s, key_index, m, r1, r2, e, u_out, v_out, batch, (cudaStream_t)stream);
 }
+
+// ---- host-buffer entry point: chunked, double-buffered H2D / decrypt / D2H on two internal streams
+static size_t host_row_in(const hqc_params *p) {
+  return (size_t)p->u_stride * 8 + (size_t)p->v_words * 8 + (size_t)p->y_stride * 4;
+}
+
+extern "C" size_t hqc_decrypt_host_workspace_bytes(const hqc_params *p, size_t chunk) {
+  if (check_level(p)) return 0;
+  const size_t per = ((size_t)p->u_stride * 8 + 15) / 16 * 16 + ((size_t)p->v_words * 8 + 15) / 16 * 16 +
+                     ((size_t)p->y_stride * 4 + 15) / 16 * 16 + ((size_t)p->k + 15) / 16 * 16;
+  return 2 * per * chunk + 4 * 256;
+}
+
+extern "C" int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, const uint64_t *v_h,
+                                      const uint32_t *y_h, uint8_t *m_h, size_t batch, void *d_work,
+                                      size_t work_bytes, size_t chunk, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  if (!u_h || !v_h || !y_h || !m_h || !d_work) return HQC_ERR_NULL;
+  if (misaligned(d_work)) return HQC_ERR_ALIGN;
+  if (chunk == 0) chunk = 8192;
+  if (chunk > batch) chunk = batch;
+  if (work_bytes < hqc_decrypt_host_workspace_bytes(p, chunk)) return HQC_ERR_SIZE;
+  (void)host_row_in;
+  const size_t ub = (size_t)p->u_stride * 8, vb = (size_t)p->v_words * 8, yb = (size_t)p->y_stride * 4;
+  auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  uint8_t *base = static_cast<uint8_t *>(d_work);
+  uint8_t *buf[2][4];
+  for (int b = 0; b < 2; b++) {
+    uint8_t *q = base + b * (r16(ub) + r16(vb) + r16(yb) + r16(p->k)) * chunk;
+    buf[b][0] = q;
+    buf[b][1] = q + r16(ub) * chunk;
+    buf[b][2] = buf[b][1] + r16(vb) * chunk;
+    buf[b][3] = buf[b][2] + r16(yb) * chunk;
+  }
+  cudaStream_t caller = (cudaStream_t)stream, st[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  int rc = HQC_OK;
+  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess) {
+    rc = HQC_ERR_CUDA;
+  }
+  if (rc == HQC_OK) {
+    cudaEventRecord(start, caller);
+    cudaStreamWaitEvent(st[0], start, 0);
+    cudaStreamWaitEvent(st[1], start, 0);
+    size_t c = 0;
+    for (size_t off = 0; off < batch && rc == HQC_OK; off += chunk, c++) {
+      const size_t n = batch - off < chunk ? batch - off : chunk;
+      const int b = (int)(c & 1);
+      cudaStream_t sb = st[b];
+      if (cudaMemcpyAsync(buf[b][0], reinterpret_cast<const uint8_t *>(u_h) + off * ub, n * ub,
+                          cudaMemcpyHostToDevice, sb) != cudaSuccess ||
+          cudaMemcpyAsync(buf[b][1], reinterpret_cast<const uint8_t *>(v_h) + off * vb, n * vb,
+                          cudaMemcpyHostToDevice, sb) != cudaSuccess ||
+          cudaMemcpyAsync(buf[b][2], reinterpret_cast<const uint8_t *>(y_h) + off * yb, n * yb,
+                          cudaMemcpyHostToDevice, sb) != cudaSuccess) {
+        rc = HQC_ERR_CUDA;
+        break;
+      }
+      rc = hqc_decrypt_batch(p, reinterpret_cast<const uint64_t *>(buf[b][0]),
+                             reinterpret_cast<const uint64_t *>(buf[b][1]),
+                             reinterpret_cast<const uint32_t *>(buf[b][2]), buf[b][3], n, (void *)sb);
+      if (rc == HQC_OK && cudaMemcpyAsync(m_h + off * p->k, buf[b][3], n * p->k, cudaMemcpyDeviceToHost, sb) !=
+                              cudaSuccess)
+        rc = HQC_ERR_CUDA;
+    }
+    cudaEventRecord(done[0], st[0]);
+    cudaEventRecord(done[1], st[1]);
+    cudaStreamWaitEvent(caller, done[0], 0);
+    cudaStreamWaitEvent(caller, done[1], 0);
+  }
+  for (int b = 0; b < 2; b++) {
+    if (st[b]) cudaStreamDestroy(st[b]);  // deferred until its work completes
+    if (done[b]) cudaEventDestroy(done[b]);
+  }
+  if (start) cudaEventDestroy(start);
+  return rc;
+}

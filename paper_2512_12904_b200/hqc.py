@@ -76,6 +76,10 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.argtypes = args
             f.restype = i32
+        L.hqc_decrypt_host_workspace_bytes.argtypes = [P, sz]
+        L.hqc_decrypt_host_workspace_bytes.restype = sz
+        L.hqc_decrypt_batch_host.argtypes = [P, vp, vp, vp, vp, sz, vp, sz, sz, vp]
+        L.hqc_decrypt_batch_host.restype = i32
         L.hqc_status_str.argtypes = [i32]
         L.hqc_status_str.restype = ctypes.c_char_p
         _lib = L
@@ -196,3 +200,28 @@ def hqc_encrypt_batch(level: int, h, s, key_index, m, r1, r2, e, u_out, v_out, s
     assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
     _check(lib().hqc_encrypt_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(key_index), _ptr(m), _ptr(r1),
                                    _ptr(r2), _ptr(e), _ptr(u_out), _ptr(v_out), B, _stream(stream)))
+
+
+def hqc_decrypt_host_workspace_bytes(level: int, chunk: int) -> int:
+    return int(lib().hqc_decrypt_host_workspace_bytes(ctypes.byref(_cp(level)), chunk))
+
+
+def _hptr(t):
+    if t.is_cuda:
+        raise HqcError("hqc_decrypt_batch_host takes host (CPU) tensors for u, v, y, m")
+    if not t.is_contiguous():
+        raise HqcError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def hqc_decrypt_batch_host(level: int, u, v, y_support, m_out, workspace, chunk: int = 0, stream=None) -> None:
+    """The end-to-end call: host (ideally pinned) u, v, y in, host m out; the library pipelines the
+    copies and the fused kernel over two internal streams. workspace: a CUDA tensor of at least
+    hqc_decrypt_host_workspace_bytes(level, chunk) bytes."""
+    p = params(level)
+    B = _rows(u, 8 * p.u_stride, "u")
+    assert _rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B
+    assert _rows(m_out, p.k, "m_out") == B
+    wb = workspace.numel() * workspace.element_size()
+    _check(lib().hqc_decrypt_batch_host(ctypes.byref(_cp(level)), _hptr(u), _hptr(v), _hptr(y_support), _hptr(m_out),
+                                        B, _ptr(workspace), wb, chunk, _stream(stream)))

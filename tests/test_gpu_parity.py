@@ -274,3 +274,20 @@ print("ok")
     env = dict(os.environ, HQC_DEC_KERNEL=kernel)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("level,chunk", [(1, 0), (3, 100), (5, 64)])
+def test_host_buffer_entry_point(level, chunk):
+    """hqc_decrypt_batch_host (host buffers, chunked over two streams) = oracle, ragged last chunk."""
+    W = valid_batch(level, 50_000, 333)
+    p = hqc.params(level)
+    hu, hv, hy = (torch.from_numpy(np.ascontiguousarray(W[k]).view(np.uint8)).pin_memory() for k in ("u", "v", "y"))
+    hm = torch.zeros(333 * p.k, dtype=torch.uint8).pin_memory()
+    ws = torch.empty(hqc.hqc_decrypt_host_workspace_bytes(level, chunk or 8192), dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch_host(level, hu, hv, hy, hm, ws, chunk)
+    torch.cuda.synchronize()
+    ref = oracle.decrypt_batch(W["params"], W["u"], W["v"], W["y"])
+    assert (hm.numpy().reshape(333, p.k) == ref).all()
+    small = torch.empty(16, dtype=torch.uint8, device=DEV)
+    with pytest.raises(hqc.HqcError):
+        hqc.hqc_decrypt_batch_host(level, hu, hv, hy, hm, small, chunk)
