@@ -292,6 +292,44 @@ def side_levels(args, dev, world, rank, hdist, hqc, skip):
     return res
 
 
+def standalone_product(args, dev, world, rank, hdist, hqc):
+    """BASELINE configs[4] second part: the standalone sparse x dense product (hqc_sparse_dense_mul_batch,
+    v = NULL) at (n, w) = (17669, 66), (35851, 100), (57637, 131), against its ALU roofline (1.5 ops
+    per (index, 32-bit word) pair) and its HBM traffic (u, y read; r written)."""
+    import torch
+
+    res = {}
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = 64 * sms * float(measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
+    for level in (1, 3, 5):
+        p = hqc.params(level)
+        B = 65536
+        i0, B = hdist.shard(rank, B)
+        u, _, y = make_inputs(level, i0, B, p)
+        du, dy = (torch.from_numpy(a.view(np.uint8)).to(dev) for a in (u, y))
+        dr = torch.empty(B * p.v_words * 8, dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            hqc.hqc_sparse_dense_mul_batch(level, du, dy, None, dr)
+        torch.cuda.synchronize()
+        steps = max(5, args.steps // 2)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            hqc.hqc_sparse_dense_mul_batch(level, du, dy, None, dr)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = hdist.max_over_ranks(e0.elapsed_time(e1), dev) / steps
+        ops = algorithmic_ops(p)
+        val = world * B / (ms / 1e3)
+        nbytes = 8 * p.u_stride + 4 * p.y_stride + 8 * p.v_words
+        res[f"n={p.n},w={p.w}"] = {"value": val, "unit": "products/s", "batch_per_gpu": B, "ms_per_step": ms,
+                                   "alu_roofline_frac": val / world * ops["stage1"] / peak,
+                                   "hbm_gbs": val / world * nbytes / 1e9,
+                                   "smem_bound_frac": val / world * ops["pairs"] / (peak / 2)}
+        del du, dy, dr
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,6 +448,7 @@ def main():
                       "samples": c["samples"], "source": "NVML, 2 ms period, timed region only"}}
     if not args.no_levels:
         out["levels"] = side_levels(args, dev, world, rank, hdist, hqc, skip=args.level)
+        out["standalone_product"] = standalone_product(args, dev, world, rank, hdist, hqc)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         got = hm.numpy().reshape(B, p.k)
         u = hu.numpy().view(np.uint64).reshape(B, -1)

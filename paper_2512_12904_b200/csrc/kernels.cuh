@@ -20,6 +20,24 @@
 
 namespace hqc {
 
+#ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (scripts/exp_variants.py)
+__device__ unsigned long long g_phase_cycles[16];
+#define PHASE_T0() long long _t = clock64()
+#define PHASE(i) do { long long _n = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _t)); _t = _n; } while (0)
+#define HQC_CAT2(a, b) a##b
+#define HQC_CAT(a, b) HQC_CAT2(a, b)
+extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *host8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host8, g_phase_cycles, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -5;
+}
+#else
+#define PHASE_T0()
+#define PHASE(i)
+#endif
+
+
 // ------------------------------------------------------------------------------------------------
 // Shared-memory carve-up of the fused / stage-1 kernels (per warp), 16-byte aligned pieces.
 template <class P> struct WarpSmem {
@@ -222,6 +240,181 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
   }
 }
 
+
+// K4b: fused decrypt, WARP-SPECIALISED. CTA = 4 warps:
+//   warps 0-1 (product pair): per ciphertext, build E from the TMA-staged u, run the rotate-and-XOR
+//     over half of the support indices each, XOR their accumulators into a ring slot that TMA has
+//     pre-filled with v (slot = v ^ acc1 ^ acc0 = r), then hand the slot over (mbarrier "full"); the
+//     next ciphertext's u, y are fetched right after E is built.
+//   warp 2 (RM decoder): per ciphertext, stage 2 on the slot (lane per RM block), symbols into one of
+//     two [n1][32] chunk buffers, slot released (mbarrier "empty").
+//   warp 3 (RS decoder): per chunk of 32 ciphertexts, stage 3 (lane per ciphertext).
+// The product warps never leave the shared-memory-bound loop for RM/RS work, so the LSU stays fed
+// while the decoders use the ALU/FMA pipes; the two-deep rings absorb the decoders' burstiness.
+template <class P> struct WsSmem {
+  using S = DecShape<P>;
+  static constexpr uint32_t E_BYTES = round_up(S::E_WORDS * 4, 16);
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t STG_BYTES = round_up(UB, 16) + round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t SLOT_BYTES = round_up(VB, 16);
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 32, 16);
+  static constexpr uint32_t SCR_BYTES = round_up(S3Scratch<P>::BYTES, 16);
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + 2 * SLOT_BYTES + 2 * SYM_BYTES + SCR_BYTES + 128;
+  static constexpr uint32_t W0 = (P::W / 2) & ~1u;
+};
+
+#ifndef HQC_DEC_MINCTAS_WS
+#define HQC_DEC_MINCTAS_WS (P::level == 5 ? 3 : 6)
+#endif
+
+template <class P>
+__global__ void __launch_bounds__(128, HQC_DEC_MINCTAS_WS) k_decrypt_ws(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out, size_t batch,
+                                                                        size_t per) {
+  using S = DecShape<P>;
+  using M = WsSmem<P>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  uint8_t *b0 = smem + GF_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(b0);
+  uint32_t *stg_u = reinterpret_cast<uint32_t *>(b0 + M::E_BYTES);
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(b0 + M::E_BYTES + round_up(M::UB, 16));
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(b0 + M::E_BYTES + M::STG_BYTES);
+  uint8_t *slots = b0 + M::E_BYTES + M::STG_BYTES + M::D_BYTES;
+  uint8_t *symb = slots + 2 * M::SLOT_BYTES;  // [2][n1][32]
+  uint16_t *scr = reinterpret_cast<uint16_t *>(symb + 2 * M::SYM_BYTES);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(scr) + M::SCR_BYTES);
+  uint64_t *bar_u = bars;            // u, y of the next ciphertext
+  uint64_t *bar_full = bars + 1;     // [2]: slot holds r
+  uint64_t *bar_empty = bars + 3;    // [2]: slot free
+  uint64_t *bar_v = bars + 5;        // [2]: v landed in the slot
+  uint64_t *bar_sfull = bars + 7;    // [2]: symbol chunk complete
+  uint64_t *bar_sempty = bars + 9;   // [2]: symbol chunk consumed
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  gf_tables_to_smem(gf);
+  if (tid == 0) {
+    mbar_init(bar_u, 1);
+    for (int s = 0; s < 2; s++) {
+      mbar_init(bar_full + s, 1);
+      mbar_init(bar_empty + s, 1);
+      mbar_init(bar_v + s, 1);
+      mbar_init(bar_sfull + s, 1);
+      mbar_init(bar_sempty + s, 1);
+    }
+  }
+  __syncthreads();
+  const size_t lo = (size_t)blockIdx.x * per;
+  const size_t hi = lo + per < batch ? lo + per : batch;
+
+  if (wid < 2) {
+    // ------------------------------------------------------------------ product pair
+    const int ptid = tid;  // 0..63
+    uint32_t ph_u = 0, ph_empty[2] = {1u, 1u}, ph_v[2] = {0u, 0u};
+    auto issue_uy = [&](size_t ct) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar_u, M::UB + M::YB);
+      tma_load_1d(stg_u, u + ct * P::U_STRIDE, M::UB, bar_u);
+      tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar_u);
+    };
+    if (lo < hi && ptid == 0) issue_uy(lo);
+    const uint32_t j0 = wid ? M::W0 : 0u, j1 = wid ? P::W : M::W0;
+    for (size_t ct = lo; ct < hi; ct++) {
+      const int s = (int)((ct - lo) & 1);
+      uint32_t *slot = reinterpret_cast<uint32_t *>(slots + s * M::SLOT_BYTES);
+      PHASE_T0();
+      mbar_wait(bar_u, ph_u);
+      ph_u ^= 1u;
+      PHASE(8);
+      s1_stage_d<P, S, 64>(stg_y, dsm, ptid);
+      s1_build_E<P, S, 64>(stg_u, E, ptid);
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      PHASE(9);
+      if (ptid == 0) {
+        if (ct + 1 < hi) issue_uy(ct + 1);      // the staging buffer is free once E is built
+        mbar_wait(bar_empty + s, ph_empty[s]);  // the RM decoder has released this slot
+        fence_proxy_async_smem();
+        mbar_expect_tx(bar_v + s, M::VB);
+        tma_load_1d(slot, v + ct * P::V_WORDS, M::VB, bar_v + s);
+      }
+      ph_empty[s] ^= 1u;
+      PHASE(10);
+      uint32_t acc[S::R];
+      s1_product_range<P, S>(E, dsm, acc, lane, j0, j1);
+      PHASE(11);
+      mbar_wait(bar_v + s, ph_v[s]);
+      ph_v[s] ^= 1u;
+      if (wid == 1) s1_xor_into<S>(acc, slot, lane);
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // also: both warps are done reading E
+      if (wid == 0) {
+        s1_xor_into<S>(acc, slot, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_full + s);  // release: the slot now holds r
+      }
+      PHASE(12);
+    }
+  } else if (wid == 2) {
+    // ------------------------------------------------------------------ RM decoder (stage 2)
+    uint32_t ph_full[2] = {0u, 0u}, ph_sempty[2] = {1u, 1u};
+    uint32_t col = 0, b = 0;
+    uint8_t *sym = symb;
+    for (size_t ct = lo; ct < hi; ct++) {
+      const int s = (int)((ct - lo) & 1);
+      if (col == 0) {  // starting a chunk: wait until the RS decoder is done with this buffer
+        mbar_wait(bar_sempty + b, ph_sempty[b]);
+        ph_sempty[b] ^= 1u;
+        sym = symb + b * M::SYM_BYTES;
+      }
+      const uint32_t *r = reinterpret_cast<const uint32_t *>(slots + s * M::SLOT_BYTES);
+      PHASE_T0();
+      mbar_wait(bar_full + s, ph_full[s]);
+      ph_full[s] ^= 1u;
+      PHASE(13);
+      for (uint32_t j = lane; j < P::N1; j += 32) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(r) + j * (P::N2 / 128);
+        uint32_t X[P::MULT * 4];
+#pragma unroll
+        for (int c = 0; c < (int)P::MULT; c++) {
+          const uint4 x = src[c];
+          X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+        }
+        sym[j * 32 + col] = (uint8_t)rm_decode_block<P::MULT>(X);
+      }
+      __syncwarp();
+      PHASE(14);
+      if (lane == 0) mbar_arrive(bar_empty + s);
+      if (++col == 32 || ct + 1 == hi) {
+        for (uint32_t e = lane; e < P::N1 * 32; e += 32)
+          if ((e & 31) >= col) sym[e] = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_sfull + b);
+        col = 0;
+        b ^= 1u;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ RS decoder (stage 3)
+    uint32_t ph_sfull[2] = {0u, 0u};
+    uint32_t b = 0;
+    for (size_t base = lo; base < hi; base += 32) {
+      const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
+      PHASE_T0();
+      mbar_wait(bar_sfull + b, ph_sfull[b]);
+      ph_sfull[b] ^= 1u;
+      PHASE(15);
+      const uint8_t *sym = symb + b * M::SYM_BYTES;
+      const bool act = (uint32_t)lane < rows;
+      auto sym_at = [&](int j) -> uint32_t { return sym[j * 32 + lane]; };
+      rs_decode_lane<P>(sym_at, gf, scr, lane, act ? m_out + (base + lane) * P::K : nullptr);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_sempty + b);
+      b ^= 1u;
+    }
+  }
+}
+
 // K4: fused decrypt, one warp PAIR (one 64-thread CTA) per ciphertext at a time. The pair shares the
 // ciphertext's doubled-u copy E: both warps build it, each warp runs the rotate-and-XOR over half of
 // the support indices, warp 1 hands its accumulators to warp 0 through shared memory, warp 0 adds v
@@ -263,22 +456,6 @@ template <class P, uint32_t EW> struct EBuildShape {
   static constexpr uint32_t E_WORDS = EW;
 };
 
-#ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (scripts/exp_variants.py)
-__device__ unsigned long long g_phase_cycles[8];
-#define PHASE_T0() long long _t = clock64()
-#define PHASE(i) do { long long _n = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _t)); _t = _n; } while (0)
-#define HQC_CAT2(a, b) a##b
-#define HQC_CAT(a, b) HQC_CAT2(a, b)
-extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *host8) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(host8, g_phase_cycles, sizeof(unsigned long long) * 8);
-  unsigned long long z[8] = {0};
-  return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -5;
-}
-#else
-#define PHASE_T0()
-#define PHASE(i)
-#endif
 // Register cap per level (minimum resident CTAs): the fused kernel is latency-bound at the occupancy
 // its register count allows, so the cap trades a few registers for more resident warp pairs.
 template <class P> struct DecOcc {
@@ -409,6 +586,7 @@ struct DevInfo {
   int sms = 0;
   int cap_decrypt[6] = {0};     // resident CTAs/SM of k_decrypt per level
   int cap_decrypt_w1[6] = {0};  // resident CTAs/SM of k_decrypt_w1 per level
+  int cap_decrypt_ws[6] = {0};  // resident CTAs/SM of k_decrypt_ws per level
   int cap_stage1[6] = {0};
   bool ready[6] = {false};
 };
@@ -421,18 +599,19 @@ constexpr int DEC_THREADS = 64;   // fused kernel: one warp pair per CTA
 
 template <class P> static uint32_t decrypt_smem() { return GF_BYTES + PairSmem<P>::BYTES; }
 template <class P> static uint32_t decrypt_w1_smem() { return GF_BYTES + WarpSmem<P>::BYTES; }
+template <class P> static uint32_t decrypt_ws_smem() { return GF_BYTES + WsSmem<P>::BYTES; }
 
-// Which fused kernel a level uses (measured, profiles/r01/NOTES.md); HQC_DEC_KERNEL=1|2 overrides
-// (experiments only).
-template <class P> static bool use_pair() {
+// Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
+// 2 = warp pair, 3 = warp-specialised. HQC_DEC_KERNEL=1|2|3 overrides (experiments and tests).
+template <class P> static int dec_kernel() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  if (env == 1) return false;
-  if (env == 2) return true;
-  return P::level != 5;
+  if (env >= 1 && env <= 3) return env;
+  return P::level == 5 ? 1 : 2;
 }
+template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
@@ -452,6 +631,9 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaFuncSetAttribute(k_decrypt_w1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_w1_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_w1<P>, 32, decrypt_w1_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt_w1[P::level] = c > 0 ? c : 1;
+  if ((e = cudaFuncSetAttribute(k_decrypt_ws<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_ws_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_ws<P>, 128, decrypt_ws_smem<P>())) != cudaSuccess) return e;
+  di.cap_decrypt_ws[P::level] = c > 0 ? c : 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   di.ready[P::level] = true;
@@ -469,9 +651,10 @@ static int cur_device(DevInfo **out) {
 // least MIN_PER ciphertexts (the lane-per-ciphertext RS stage wants full chunks).
 constexpr size_t MIN_PER = 32;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
-  const bool pair = use_pair<P>();
-  const size_t cap = (size_t)di.sms * (pair ? di.cap_decrypt[P::level] : di.cap_decrypt_w1[P::level]);
-  const size_t min_per = pair ? MIN_PER : MIN_PER / 2;
+  const int kind = dec_kernel<P>();
+  const int c = kind == 1 ? di.cap_decrypt_w1[P::level] : kind == 2 ? di.cap_decrypt[P::level] : di.cap_decrypt_ws[P::level];
+  const size_t cap = (size_t)di.sms * c;
+  const size_t min_per = kind == 1 ? MIN_PER / 2 : kind == 2 ? MIN_PER : 2 * MIN_PER;
   size_t ctas = (batch + min_per - 1) / min_per;
   if (ctas > cap) ctas = cap;
   if (ctas == 0) ctas = 1;
@@ -488,10 +671,11 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
   int grid;
   size_t per;
   decrypt_shape<P>(*di, batch, &grid, &per);
-  if (use_pair<P>())
-    k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per);
-  else
-    k_decrypt_w1<P><<<grid, 32, decrypt_w1_smem<P>(), st>>>(u, v, y, m, batch, per);
+  switch (dec_kernel<P>()) {
+    case 1: k_decrypt_w1<P><<<grid, 32, decrypt_w1_smem<P>(), st>>>(u, v, y, m, batch, per); break;
+    case 2: k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per); break;
+    default: k_decrypt_ws<P><<<grid, 128, decrypt_ws_smem<P>(), st>>>(u, v, y, m, batch, per); break;
+  }
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
@@ -563,7 +747,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
-  *wpc = use_pair<P>() ? DEC_THREADS / 32 : 1;
+  *wpc = dec_kernel<P>() == 1 ? 1 : dec_kernel<P>() == 2 ? DEC_THREADS / 32 : 4;
   return HQC_OK;
 }
 

@@ -19,6 +19,15 @@
 
 namespace hqc {
 
+// index-pair loop unroll per level, from scripts/exp_unroll.py (2: -0.5% HQC-1/3; 3: -2.4% HQC-5)
+template <class P> constexpr int s1_unroll() {
+#ifdef HQC_S1_UNROLL
+  return HQC_S1_UNROLL;
+#else
+  return P::level == 5 ? 3 : 2;
+#endif
+}
+
 // Build E (S::E_WORDS words) from the staged dense row su (shared memory).
 template <class P, class S, int NT = 32>
 __device__ __forceinline__ void s1_build_E(const uint32_t *su, uint32_t *E, int lane) {
@@ -61,7 +70,8 @@ __device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32
   for (int k = 0; k < R; k++) acc[k] = 0;
   const uint32_t *Eb = E + lane * R;
   uint32_t j = j0;
-#pragma unroll 1
+  constexpr int kUnroll = s1_unroll<P>();
+#pragma unroll kUnroll
   for (; j + 1 < j1; j += 2) {  // two indices per pass: one 3-input XOR per word
     const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
     const uint32_t *p0 = Eb + (dd.x >> 5);
@@ -118,6 +128,14 @@ __device__ __forceinline__ void s1_store_r_xor2(const uint32_t (&acc)[S::R], uin
 #pragma unroll
   for (int k = 0; k < (int)S::R; k++)
     if (lane * S::R + k < S::NOUT) rsm[lane * S::R + k] = acc[k] ^ xs[lane * S::R + k] ^ sv[lane * S::R + k];
+}
+
+// In-place XOR of the accumulators into a buffer (rsm[lane*R + k] ^= acc[k]); R odd: conflict-free.
+template <class S>
+__device__ __forceinline__ void s1_xor_into(const uint32_t (&acc)[S::R], uint32_t *rsm, int lane) {
+#pragma unroll
+  for (int k = 0; k < (int)S::R; k++)
+    if (lane * S::R + k < S::NOUT) rsm[lane * S::R + k] ^= acc[k];
 }
 
 // r ^= v with v staged in shared memory (16-byte chunks).

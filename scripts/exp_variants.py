@@ -9,7 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VAR = {"full": 0, "no_s2": 1, "no_s3": 2, "no_s2s3": 3}
 PHASES = ["wait_uy", "stage_d+buildE+sync", "product", "sync_after_product", "combine+wait_v+store",
-          "stage2", "sync_after_stage2", "stage3"]
+          "stage2", "sync_after_stage2", "stage3",
+          "ws.P.wait_u", "ws.P.build", "ws.P.wait_empty", "ws.P.product", "ws.P.combine",
+          "ws.D.wait_full", "ws.D.stage2", "ws.Q.wait_sfull"]
 
 
 def build():
@@ -39,14 +41,12 @@ def timing():
         du, dv, dy = (torch.from_numpy(a.view(np.uint8)).cuda() for a in (u, v, y))
         dm = torch.empty(B * p.k, dtype=torch.uint8, device="cuda")
         f = getattr(L, f"hqc_exp_phases_l{level}")
-        buf = (ctypes.c_ulonglong * 8)()
+        buf = (ctypes.c_ulonglong * 16)()
         hqc.hqc_decrypt_batch(level, du, dv, dy, dm)
         f(buf)
         hqc.hqc_decrypt_batch(level, du, dv, dy, dm)
         f(buf)
-        tot = sum(buf)
-        out[level] = {PHASES[i]: round(100.0 * buf[i] / tot, 1) for i in range(8)}
-        out[level]["total_warp_cycles_per_ct"] = round(tot / B, 0)
+        out[level] = {PHASES[i]: round(buf[i] / B, 0) for i in range(16) if buf[i]}
     print(json.dumps(out))
 
 

@@ -244,7 +244,7 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
     """The library picks the warp-pair kernel (HQC-1/3) or the one-warp kernel (HQC-5) per level;
     HQC_DEC_KERNEL forces either (read once per process), so each runs in a subprocess on every level."""
