@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym,
 #define HQC_DEC_MINCTAS (P::level == 5 ? 6 : (P::level == 1 ? 14 : 8))
 #endif
 #ifndef HQC_DEC_MINCTAS_W1
-#define HQC_DEC_MINCTAS_W1 (P::level == 5 ? 12 : 20)
+#define HQC_DEC_MINCTAS_W1 (P::level == 5 ? 14 : (P::level == 1 ? 16 : 12))
 #endif
 
 // K4a: fused decrypt, one warp per ciphertext (the pair-free variant). Warp g owns ciphertexts
@@ -609,7 +609,7 @@ template <class P> static int dec_kernel() {
     return s ? atoi(s) : 0;
   }();
   if (env >= 1 && env <= 3) return env;
-  return P::level == 5 ? 1 : 2;
+  return P::level == 3 ? 2 : 1;  // occupancy sweeps: one warp wins for HQC-1 (0.629 vs 0.645 ms) and HQC-5
 }
 template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }

@@ -6,7 +6,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VALUES = [6, 7, 8, 9, 10, 11, 12, 14]
+VALUES = [int(x) for x in os.environ.get("OCC_VALUES", "6,7,8,9,10,11,12,14").split(",")]
+MACRO = os.environ.get("OCC_MACRO", "HQC_DEC_MINCTAS")
 
 
 def build():
@@ -15,7 +16,7 @@ def build():
     from paper_2512_12904_b200 import build as b
 
     def one(m):
-        return b.build_variant(os.path.join(ROOT, "scripts", f"libhqc_occ_{m}.so"), [f"HQC_DEC_MINCTAS={m}"])
+        return b.build_variant(os.path.join(ROOT, "scripts", f"libhqc_occ_{m}.so"), [f"{MACRO}={m}"])
 
     with ThreadPoolExecutor(4) as ex:
         list(ex.map(one, VALUES))
