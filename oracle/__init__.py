@@ -18,7 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["params.c", "gf256.c", "ring.c", "rm.c", "rs.c", "pke.c", "batch.c"]
+_SOURCES = ["params.c", "gf256.c", "ring.c", "rm.c", "rs.c", "pke.c", "shake.c", "kem.c", "batch.c"]
 
 
 def build(force: bool = False) -> str:
@@ -98,6 +98,15 @@ def lib():
             "orc_stage1_batch": (None, [P(_Params), c_p, sz, c_p, sz, c_p, sz, c_p, sz, sz, i32]),
             "orc_rm_decode_batch": (None, [P(_Params), c_p, sz, c_p, sz, sz, i32]),
             "orc_rs_decode_batch": (None, [P(_Params), c_p, sz, c_p, sz, c_p, sz, i32]),
+            "orc_keccak_f1600": (None, [c_p]),
+            "orc_shake256": (None, [c_p, sz, c_p, sz]),
+            "orc_sample_fixed_weight": (None, [c_p, u32, u32, c_p]),
+            "orc_kem_hpk": (None, [P(_Params), c_p, c_p, c_p]),
+            "orc_kem_coins": (None, [P(_Params), c_p, c_p, c_p, c_p, c_p]),
+            "orc_kem_encaps": (None, [P(_Params), c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+            "orc_kem_decaps": (i32, [P(_Params), c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+            "orc_kem_decaps_batch": (None, [P(_Params), c_p, c_p, sz, c_p, c_p, c_p, c_p, sz, c_p, sz, c_p, sz, c_p,
+                                            c_p, sz, i32]),
             "orc_encrypt_batch": (
                 None,
                 [P(_Params), c_p, sz, c_p, sz, c_p, c_p, sz, c_p, c_p, c_p, sz, c_p, sz, c_p, sz, sz, i32],
@@ -318,3 +327,84 @@ def encrypt_batch(p: Params, h, s, key_of_row, m, r1, r2, e, nthreads: int | Non
                             _ptr(key_of_row), _ptr(m), m.shape[1], _ptr(r1), _ptr(r2), _ptr(e),
                             r1.shape[1], _ptr(u), p.words, _ptr(v), p.vwords, B, _threads(nthreads))
     return u, v
+
+
+# ---------------- KEM row (SHAKE256, sampler, HHK) ----------------
+def shake256(msg: bytes, outlen: int) -> bytes:
+    m = np.frombuffer(bytes(msg), dtype=np.uint8).copy() if len(msg) else np.zeros(1, np.uint8)
+    out = np.zeros(max(outlen, 1), np.uint8)
+    lib().orc_shake256(_ptr(m), len(msg), _ptr(out), outlen)
+    return out[:outlen].tobytes()
+
+
+def keccak_f1600(state) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(state, dtype=np.uint64).copy())
+    lib().orc_keccak_f1600(_ptr(a))
+    return a
+
+
+def sample_fixed_weight(rnd: bytes, n: int, w: int) -> np.ndarray:
+    r = np.frombuffer(bytes(rnd), dtype=np.uint8).copy()
+    assert r.size >= 4 * w
+    out = np.zeros(w, np.uint32)
+    lib().orc_sample_fixed_weight(_ptr(r), n, w, _ptr(out))
+    return out
+
+
+def kem_hpk(p: Params, h, s) -> bytes:
+    h = np.ascontiguousarray(h[: p.words], dtype=np.uint64)
+    s = np.ascontiguousarray(s[: p.words], dtype=np.uint64)
+    out = np.zeros(32, np.uint8)
+    lib().orc_kem_hpk(ctypes.byref(p._c()), _ptr(h), _ptr(s), _ptr(out))
+    return out.tobytes()
+
+
+def kem_coins(p: Params, hpk: bytes, m):
+    hp = np.frombuffer(hpk, np.uint8).copy()
+    m = np.ascontiguousarray(np.asarray(m, dtype=np.uint8)[: p.k])
+    r = np.zeros((3, p.wr), np.uint32)
+    lib().orc_kem_coins(ctypes.byref(p._c()), _ptr(hp), _ptr(m), _ptr(r[0]), _ptr(r[1]), _ptr(r[2]))
+    return r[0], r[1], r[2]
+
+
+def kem_encaps(p: Params, h, s, hpk: bytes, m):
+    h = np.ascontiguousarray(h[: p.words], dtype=np.uint64)
+    s = np.ascontiguousarray(s[: p.words], dtype=np.uint64)
+    hp = np.frombuffer(hpk, np.uint8).copy()
+    m = np.ascontiguousarray(np.asarray(m, dtype=np.uint8)[: p.k])
+    u = np.zeros(p.words, np.uint64)
+    v = np.zeros(p.vwords, np.uint64)
+    K = np.zeros(64, np.uint8)
+    lib().orc_kem_encaps(ctypes.byref(p._c()), _ptr(h), _ptr(s), _ptr(hp), _ptr(m), _ptr(u), _ptr(v), _ptr(K))
+    return u, v, K.tobytes()
+
+
+def kem_decaps(p: Params, h, s, hpk: bytes, y, sigma, u, v):
+    h = np.ascontiguousarray(h[: p.words], dtype=np.uint64)
+    s = np.ascontiguousarray(s[: p.words], dtype=np.uint64)
+    hp = np.frombuffer(hpk, np.uint8).copy()
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.uint32)[: p.w])
+    sg = np.ascontiguousarray(np.asarray(sigma, dtype=np.uint8)[: p.k])
+    u = np.ascontiguousarray(u[: p.words], dtype=np.uint64)
+    v = np.ascontiguousarray(v[: p.vwords], dtype=np.uint64)
+    K = np.zeros(64, np.uint8)
+    ok = lib().orc_kem_decaps(ctypes.byref(p._c()), _ptr(h), _ptr(s), _ptr(hp), _ptr(y), _ptr(sg), _ptr(u), _ptr(v),
+                              _ptr(K))
+    return K.tobytes(), bool(ok)
+
+
+def kem_decaps_batch(p: Params, h, s, hpk, sigma, key_of_row, y, u, v, nthreads=None):
+    h, s = _rows(h, np.uint64), _rows(s, np.uint64)
+    assert h.shape == s.shape
+    hpk = np.ascontiguousarray(hpk, dtype=np.uint8)
+    sigma = np.ascontiguousarray(sigma, dtype=np.uint8)
+    assert sigma.shape[1] == p.k and hpk.shape[1] == 32
+    key_of_row = np.ascontiguousarray(key_of_row, dtype=np.int64)
+    y, u, v = _rows(y, np.uint32), _rows(u, np.uint64), _rows(v, np.uint64)
+    B = u.shape[0]
+    K = np.zeros((B, 64), np.uint8)
+    acc = np.zeros(B, np.uint8)
+    lib().orc_kem_decaps_batch(ctypes.byref(p._c()), _ptr(h), _ptr(s), h.shape[1], _ptr(hpk), _ptr(sigma),
+                               _ptr(key_of_row), _ptr(y), y.shape[1], _ptr(u), u.shape[1], _ptr(v), v.shape[1],
+                               _ptr(K), _ptr(acc), B, _threads(nthreads))
+    return K, acc

@@ -11,12 +11,12 @@ typedef struct {
   const orc_params *p;
   const void *a0, *a1, *a2, *a3, *a4, *a5, *a6;
   size_t s0, s1, s2, s3, s4, s5, s6;
-  void *o0, *o1, *o2;
+  void *o0, *o1, *o2;  /* K_DECAP passes v (input) through o2 */
   size_t os0, os1;
   size_t lo, hi;
 } job_t;
 
-enum { K_DEC, K_ENC, K_RM, K_RS, K_ST1 };
+enum { K_DEC, K_ENC, K_RM, K_RS, K_ST1, K_DECAP };
 
 static void *worker(void *arg) {
   job_t *j = (job_t *)arg;
@@ -42,6 +42,15 @@ static void *worker(void *arg) {
         int ok = orc_rs_decode((const uint8_t *)j->a0 + i * j->s0, p->n1, p->k, p->delta,
                                (uint8_t *)j->o0 + i * j->os0);
         if (j->o1) ((uint8_t *)j->o1)[i] = (uint8_t)ok;
+        break;
+      }
+      case K_DECAP: {
+        int64_t key = ((const int64_t *)j->a4)[i];
+        int acc = orc_kem_decaps(p, (const uint64_t *)j->a0 + key * j->s0, (const uint64_t *)j->a1 + key * j->s0,
+                                 (const uint8_t *)j->a2 + key * 32, (const uint32_t *)j->a5 + i * j->s5,
+                                 (const uint8_t *)j->a3 + key * p->k, (const uint64_t *)j->a6 + i * j->s6,
+                                 (const uint64_t *)j->o2 + i * j->os1, (uint8_t *)j->o0 + i * 64);
+        if (j->o1) ((uint8_t *)j->o1)[i] = (uint8_t)acc;
         break;
       }
       case K_ENC: {
@@ -119,5 +128,18 @@ void orc_encrypt_batch(const orc_params *p, const uint64_t *h, size_t h_stride,
   j.a0 = h; j.s0 = h_stride; j.a1 = s; j.s1 = s_stride; j.a2 = key_of_row;
   j.a3 = m; j.s3 = m_stride; j.a4 = r1; j.a5 = r2; j.a6 = e; j.s4 = sup_stride;
   j.o0 = u; j.os0 = u_stride; j.o1 = v; j.os1 = v_stride;
+  run(&j, batch, nthreads);
+}
+
+void orc_kem_decaps_batch(const orc_params *p, const uint64_t *h, const uint64_t *s, size_t key_stride,
+                          const uint8_t *hpk, const uint8_t *sigma, const int64_t *key_of_row,
+                          const uint32_t *y, size_t y_stride, const uint64_t *u, size_t u_stride,
+                          const uint64_t *v, size_t v_stride, uint8_t *K, uint8_t *acc, size_t batch,
+                          int nthreads) {
+  job_t j = {0};
+  j.kind = K_DECAP; j.p = p;
+  j.a0 = h; j.a1 = s; j.s0 = key_stride; j.a2 = hpk; j.a3 = sigma; j.a4 = key_of_row;
+  j.a5 = y; j.s5 = y_stride; j.a6 = u; j.s6 = u_stride;
+  j.o2 = (void *)v; j.os1 = v_stride; j.o0 = K; j.o1 = acc;
   run(&j, batch, nthreads);
 }

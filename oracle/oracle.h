@@ -93,6 +93,24 @@ void orc_decrypt_stage1(const orc_params *p, const uint64_t *u, const uint64_t *
 void orc_decrypt(const orc_params *p, const uint64_t *u, const uint64_t *v, const uint32_t *y,
                  uint8_t *m);
 
+/* ---- KEM row of SURVEY §8(f) (HHK with implicit rejection; readings R#20-R#23 in DESIGN.md) ---- */
+void orc_keccak_f1600(uint64_t A[25]);
+void orc_shake256(const uint8_t *msg, size_t len, uint8_t *out, size_t outlen);
+/* w distinct positions in [0, n) from 4w bytes of PRNG output (R#22) */
+void orc_sample_fixed_weight(const uint8_t *rnd, uint32_t n, uint32_t w, uint32_t *out);
+/* serialised pk = h bytes (ceil(n/8)) || s bytes (ceil(n/8)); H_pk = SHAKE256(pk || 0x02, 32) */
+void orc_kem_hpk(const orc_params *p, const uint64_t *h, const uint64_t *s, uint8_t hpk[32]);
+/* theta = SHAKE256(H_pk || m || 0x01, 32); (r1, r2, e) = sample(SHAKE256(theta || 0x04, 12 wr)) */
+void orc_kem_coins(const orc_params *p, const uint8_t hpk[32], const uint8_t *m, uint32_t *r1, uint32_t *r2,
+                   uint32_t *e);
+/* Encaps: c = Encrypt(pk, m; coins(m)), K = SHAKE256(m || c || 0x03, 64), c = u bytes || v bytes */
+void orc_kem_encaps(const orc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t hpk[32],
+                    const uint8_t *m, uint64_t *u, uint64_t *v, uint8_t K[64]);
+/* Decaps: m' = Decrypt; c' = Encrypt(pk, m'; coins(m')); K = SHAKE256((c' == c ? m' : sigma) || c || 0x03, 64).
+   Returns 1 if the ciphertext was accepted (c' == c). */
+int orc_kem_decaps(const orc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t hpk[32],
+                   const uint32_t *y, const uint8_t *sigma, const uint64_t *u, const uint64_t *v, uint8_t K[64]);
+
 /* ---- Batched drivers (strided rows; nthreads POSIX threads, static partition) ---- */
 void orc_decrypt_batch(const orc_params *p, const uint64_t *u, size_t u_stride,
                        const uint64_t *v, size_t v_stride, const uint32_t *y, size_t y_stride,
@@ -106,6 +124,11 @@ void orc_rm_decode_batch(const orc_params *p, const uint64_t *r, size_t r_stride
                          size_t sym_stride, size_t batch, int nthreads);
 void orc_rs_decode_batch(const orc_params *p, const uint8_t *sym, size_t sym_stride,
                          uint8_t *m, size_t m_stride, uint8_t *ok, size_t batch, int nthreads);
+void orc_kem_decaps_batch(const orc_params *p, const uint64_t *h, const uint64_t *s, size_t key_stride,
+                          const uint8_t *hpk, const uint8_t *sigma, const int64_t *key_of_row,
+                          const uint32_t *y, size_t y_stride, const uint64_t *u, size_t u_stride,
+                          const uint64_t *v, size_t v_stride, uint8_t *K, uint8_t *acc, size_t batch,
+                          int nthreads);
 void orc_stage1_batch(const orc_params *p, const uint64_t *u, size_t u_stride, const uint64_t *v,
                       size_t v_stride, const uint32_t *y, size_t y_stride, uint64_t *r,
                       size_t r_stride, size_t batch, int nthreads);
