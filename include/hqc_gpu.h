@@ -136,6 +136,38 @@ int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
                       size_t batch, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * batched HQC.KEM with the HHK transform and implicit rejection (Decap
+ * "decrypts the ciphertext (calling Decrypt), and then re-encrypts to verify correctness, and
+ * securely rejects invalid ciphertexts"). The paper gives no byte-level hash inputs; this library
+ * follows DESIGN.md readings R#20-R#23 (SHAKE256 = FIPS 202 XOF; tags G=0x01, H=0x02, K=0x03,
+ * PRNG=0x04 appended to the hashed bytes):
+ *   H_pk  = SHAKE256(h bytes || s bytes || 0x02, 32)     h, s serialised as ceil(n/8) LE bytes
+ *   theta = SHAKE256(H_pk || m || 0x01, 32)
+ *   (r1, r2, e) = fixed-weight sampling of SHAKE256(theta || 0x04, 12 wr) (3 wr LE uint32 words)
+ *   c     = u bytes (ceil(n/8)) || v bytes (n1 n2 / 8)
+ *   Encaps:  (u, v) = Encrypt(pk, m; r1, r2, e),  K = SHAKE256(m || c || 0x03, 64)
+ *   Decaps:  m' = Decrypt(y, c); c' = Encrypt(pk, m'; coins(m')); K = SHAKE256((c' == c ? m' : sigma)
+ *            || c || 0x03, 64). The comparison ignores bits >= n of u (as every other entry point).
+ * Layouts: h, s [nkeys][u_stride] uint64 (rows as written by hqc_keygen_batch), hpk [nkeys][32],
+ * sigma [nkeys][k], y_support [nkeys][y_stride] (per KEY), key_index [batch] uint32 (NULL = row b
+ * uses key b), m [batch][k], u [batch][u_stride], v [batch][v_words], K_out [batch][64],
+ * accepted_out [batch] uint8 (nullable; 1 = c' == c). d_work: caller-owned device scratch of at
+ * least hqc_kem_workspace_bytes(p, batch) bytes (else HQC_ERR_SIZE); it holds m', the sampled
+ * supports and the comparison flags and may be reused once the stream has passed the call.
+ * Encaps takes m from the caller (the message draw is the caller's randomness).
+ * ------------------------------------------------------------------------------------------- */
+size_t hqc_kem_workspace_bytes(const hqc_params *p, size_t batch);
+int hqc_kem_hpk_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, uint8_t *hpk_out,
+                      size_t nkeys, void *stream);
+int hqc_kem_encaps_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t *hpk,
+                         const uint32_t *key_index, const uint8_t *m, uint64_t *u_out, uint64_t *v_out,
+                         uint8_t *K_out, size_t batch, void *d_work, size_t work_bytes, void *stream);
+int hqc_kem_decaps_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t *hpk,
+                         const uint8_t *sigma, const uint32_t *key_index, const uint32_t *y_support,
+                         const uint64_t *u, const uint64_t *v, uint8_t *K_out, uint8_t *accepted_out,
+                         size_t batch, void *d_work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Host-buffer decrypt (the end-to-end call): u_h, v_h, y_h, m_h are HOST arrays in the layouts of
  * hqc_decrypt_batch (page-locked memory recommended; pageable memory works but copies synchronously).
  * The batch is processed in chunks of `chunk` ciphertexts (0 = 8192) on two internal streams so that

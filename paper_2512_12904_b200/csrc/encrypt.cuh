@@ -153,13 +153,19 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
   }
 }
 
-// encrypt: one warp per ciphertext.
-template <class P>
+// encrypt: one warp per ciphertext. CMP = false writes (u, v) to u_out / v_out. CMP = true is the
+// KEM's re-encryption check (kem.cuh): the re-encrypted (u', v') never leaves shared memory; it is
+// compared with the received (u_cmp, v_cmp) word by word (bits >= n of u_cmp ignored, as in
+// oracle/kem.c) with no early exit, and eq_out[ct] = 1 iff every word matched.
+template <class P, bool CMP = false>
 __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
                                                 const uint32_t *__restrict__ key_index, const uint8_t *__restrict__ m,
                                                 const uint32_t *__restrict__ r1, const uint32_t *__restrict__ r2,
                                                 const uint32_t *__restrict__ e, uint64_t *__restrict__ u_out,
-                                                uint64_t *__restrict__ v_out, size_t batch) {
+                                                uint64_t *__restrict__ v_out, size_t batch,
+                                                const uint64_t *__restrict__ u_cmp = nullptr,
+                                                const uint64_t *__restrict__ v_cmp = nullptr,
+                                                uint8_t *__restrict__ eq_out = nullptr) {
   extern __shared__ __align__(16) uint8_t smem[];
   using M = EncSmem<P>;
   const int lane = threadIdx.x;
@@ -186,7 +192,16 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
     if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;
     for (uint32_t q = P::Q0 + 1 + lane; q < 2 * P::U_STRIDE; q += 32) E[q] = 0;
     __syncwarp();
-    copy_s2g(u_out + ct * P::U_STRIDE, E, 2 * P::U_STRIDE, lane);
+    uint32_t diff = 0;
+    if constexpr (CMP) {
+      const uint32_t *uc = reinterpret_cast<const uint32_t *>(u_cmp + ct * P::U_STRIDE);
+      for (uint32_t q = lane; q < 2 * P::U_WORDS; q += 32) {
+        const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & ((1u << P::C) - 1u) : 0u);
+        diff |= x ^ E[q];
+      }
+    } else {
+      copy_s2g(u_out + ct * P::U_STRIDE, E, 2 * P::U_STRIDE, lane);
+    }
     __syncwarp();
     // v = trunc(mG + s * r2 + e)
     copy_g2s(stg, s + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
@@ -205,7 +220,18 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
     __syncwarp();
     xor_support_bits(E, s_e, P::WR, P::N12, lane);
     __syncwarp();
-    copy_s2g(v_out + ct * P::V_WORDS, E, P::NW, lane);
+    if constexpr (CMP) {
+      const uint4 *vc = reinterpret_cast<const uint4 *>(v_cmp + ct * P::V_WORDS);
+      for (uint32_t c = lane; c < P::NW / 4; c += 32) {
+        const uint4 x = __ldg(vc + c);
+        const uint4 y = reinterpret_cast<const uint4 *>(E)[c];
+        diff |= (x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w);
+      }
+      diff = __reduce_or_sync(0xffffffffu, diff);
+      if (lane == 0) eq_out[ct] = diff == 0;
+    } else {
+      copy_s2g(v_out + ct * P::V_WORDS, E, P::NW, lane);
+    }
     __syncwarp();
   }
 }

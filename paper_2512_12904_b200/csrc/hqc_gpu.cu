@@ -193,6 +193,56 @@ extern "C" int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const u
   HQC_DISPATCH(p, encrypt, h, s, key_index, m, r1, r2, e, u_out, v_out, batch, (cudaStream_t)stream);
 }
 
+// ---- KEM row: kem.cuh
+extern "C" size_t hqc_kem_workspace_bytes(const hqc_params *p, size_t batch) {
+  if (check_level(p)) return 0;
+  switch (p->level) {
+    case 1: return kem_ws_l1(batch);
+    case 3: return kem_ws_l3(batch);
+    default: return kem_ws_l5(batch);
+  }
+}
+
+extern "C" int hqc_kem_hpk_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, uint8_t *hpk_out,
+                                 size_t nkeys, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (nkeys == 0) return HQC_OK;
+  if (nkeys > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(h); HQC_CHECK_PTR(s); HQC_CHECK_PTR(hpk_out);
+  HQC_DISPATCH(p, kem_hpk, h, s, hpk_out, nkeys, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_kem_encaps_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t *hpk,
+                                    const uint32_t *key_index, const uint8_t *m, uint64_t *u_out, uint64_t *v_out,
+                                    uint8_t *K_out, size_t batch, void *d_work, size_t work_bytes, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(h); HQC_CHECK_PTR(s); HQC_CHECK_PTR(hpk); HQC_CHECK_PTR(m); HQC_CHECK_PTR(u_out);
+  HQC_CHECK_PTR(v_out); HQC_CHECK_PTR(K_out); HQC_CHECK_PTR(d_work);
+  if (key_index && misaligned(key_index)) return HQC_ERR_ALIGN;
+  if (work_bytes < hqc_kem_workspace_bytes(p, batch)) return HQC_ERR_SIZE;
+  HQC_DISPATCH(p, kem_encaps, h, s, hpk, key_index, m, u_out, v_out, K_out, batch, d_work, (cudaStream_t)stream);
+}
+
+extern "C" int hqc_kem_decaps_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t *hpk,
+                                    const uint8_t *sigma, const uint32_t *key_index, const uint32_t *y_support,
+                                    const uint64_t *u, const uint64_t *v, uint8_t *K_out, uint8_t *accepted_out,
+                                    size_t batch, void *d_work, size_t work_bytes, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(h); HQC_CHECK_PTR(s); HQC_CHECK_PTR(hpk); HQC_CHECK_PTR(sigma); HQC_CHECK_PTR(y_support);
+  HQC_CHECK_PTR(u); HQC_CHECK_PTR(v); HQC_CHECK_PTR(K_out); HQC_CHECK_PTR(d_work);
+  if (key_index && misaligned(key_index)) return HQC_ERR_ALIGN;
+  if (work_bytes < hqc_kem_workspace_bytes(p, batch)) return HQC_ERR_SIZE;
+  HQC_DISPATCH(p, kem_decaps, h, s, hpk, sigma, key_index, y_support, u, v, K_out, accepted_out, batch, d_work,
+               (cudaStream_t)stream);
+}
+
 // ---- host-buffer entry point: chunked, double-buffered H2D / decrypt / D2H on two internal streams
 static size_t host_row_in(const hqc_params *p) {
   return (size_t)p->u_stride * 8 + (size_t)p->v_words * 8 + (size_t)p->y_stride * 4;

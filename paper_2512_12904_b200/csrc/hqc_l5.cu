@@ -1,6 +1,7 @@
 // Level-5 instantiation of the kernels (own translation unit: own constant bank).
 #define HQC_THIS_LEVEL 5
 #include "kernels.cuh"
+#include "kem.cuh"
 #include "launchers.h"
 
 namespace hqc {
@@ -23,4 +24,17 @@ int encrypt_l5(const uint64_t *h, const uint64_t *s, const uint32_t *key, const 
   return launch_encrypt<PL>(h, s, key, m, r1, r2, e, u, v, batch, st);
 }
 int shape_l5(size_t batch, int *grid, int *wpc) { return shape_impl<PL>(batch, grid, wpc); }
+size_t kem_ws_l5(size_t batch) { return kem_ws_bytes<PL>(batch); }
+int kem_hpk_l5(const uint64_t *h, const uint64_t *s, uint8_t *hpk, size_t nkeys, cudaStream_t st) {
+  return launch_kem_hpk<PL>(h, s, hpk, nkeys, st);
+}
+int kem_encaps_l5(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint32_t *key, const uint8_t *m,
+                   uint64_t *u, uint64_t *v, uint8_t *K, size_t batch, void *ws, cudaStream_t st) {
+  return launch_kem_encaps<PL>(h, s, hpk, key, m, u, v, K, batch, ws, st);
+}
+int kem_decaps_l5(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint8_t *sigma, const uint32_t *key,
+                   const uint32_t *y, const uint64_t *u, const uint64_t *v, uint8_t *K, uint8_t *acc, size_t batch,
+                   void *ws, cudaStream_t st) {
+  return launch_kem_decaps<PL>(h, s, hpk, sigma, key, y, u, v, K, acc, batch, ws, st);
+}
 }  // namespace hqc

@@ -17,7 +17,15 @@
   int encrypt_l##L(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m,                \
                    const uint32_t *r1, const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v,        \
                    size_t batch, cudaStream_t st);                                                              \
-  int shape_l##L(size_t batch, int *grid, int *wpc);
+  int shape_l##L(size_t batch, int *grid, int *wpc);                                                            \
+  size_t kem_ws_l##L(size_t batch);                                                                             \
+  int kem_hpk_l##L(const uint64_t *h, const uint64_t *s, uint8_t *hpk, size_t nkeys, cudaStream_t st);          \
+  int kem_encaps_l##L(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint32_t *key,            \
+                      const uint8_t *m, uint64_t *u, uint64_t *v, uint8_t *K, size_t batch, void *ws,           \
+                      cudaStream_t st);                                                                         \
+  int kem_decaps_l##L(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint8_t *sigma,           \
+                      const uint32_t *key, const uint32_t *y, const uint64_t *u, const uint64_t *v, uint8_t *K, \
+                      uint8_t *acc, size_t batch, void *ws, cudaStream_t st);
 
 namespace hqc {
 HQC_LEVEL_API(1)

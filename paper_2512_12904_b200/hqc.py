@@ -71,11 +71,16 @@ def lib() -> ctypes.CDLL:
             "hqc_decrypt_launch_shape": [P, sz, ctypes.POINTER(i32), ctypes.POINTER(i32)],
             "hqc_keygen_batch": [P, vp, vp, vp, vp, sz, vp],
             "hqc_encrypt_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
+            "hqc_kem_hpk_batch": [P, vp, vp, vp, sz, vp],
+            "hqc_kem_encaps_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, sz, vp],
+            "hqc_kem_decaps_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, sz, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = i32
+        L.hqc_kem_workspace_bytes.argtypes = [P, sz]
+        L.hqc_kem_workspace_bytes.restype = sz
         L.hqc_decrypt_host_workspace_bytes.argtypes = [P, sz]
         L.hqc_decrypt_host_workspace_bytes.restype = sz
         L.hqc_decrypt_batch_host.argtypes = [P, vp, vp, vp, vp, sz, vp, sz, sz, vp]
@@ -200,6 +205,45 @@ def hqc_encrypt_batch(level: int, h, s, key_index, m, r1, r2, e, u_out, v_out, s
     assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
     _check(lib().hqc_encrypt_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(key_index), _ptr(m), _ptr(r1),
                                    _ptr(r2), _ptr(e), _ptr(u_out), _ptr(v_out), B, _stream(stream)))
+
+
+def hqc_kem_workspace_bytes(level: int, batch: int) -> int:
+    return int(lib().hqc_kem_workspace_bytes(ctypes.byref(_cp(level)), batch))
+
+
+def _nbytes(t) -> int:
+    return t.numel() * t.element_size()
+
+
+def hqc_kem_hpk_batch(level: int, h, s, hpk_out, stream=None) -> None:
+    """H_pk = SHAKE256(h bytes || s bytes || 0x02, 32) per key (R#20-R#21)."""
+    p = params(level)
+    K = _rows(h, 8 * p.u_stride, "h")
+    assert _rows(s, 8 * p.u_stride, "s") == K and _rows(hpk_out, 32, "hpk_out") == K
+    _check(lib().hqc_kem_hpk_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk_out), K, _stream(stream)))
+
+
+def hqc_kem_encaps_batch(level: int, h, s, hpk, key_index, m, u_out, v_out, K_out, workspace, stream=None) -> None:
+    """HHK Encaps with caller-drawn messages m: coins(H_pk, m) -> Encrypt -> K (R#20-R#23)."""
+    p = params(level)
+    B = _rows(m, p.k, "m")
+    assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
+    assert _rows(K_out, 64, "K_out") == B
+    _check(lib().hqc_kem_encaps_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk), _ptr(key_index), _ptr(m),
+                                      _ptr(u_out), _ptr(v_out), _ptr(K_out), B, _ptr(workspace), _nbytes(workspace),
+                                      _stream(stream)))
+
+
+def hqc_kem_decaps_batch(level: int, h, s, hpk, sigma, key_index, y_support, u, v, K_out, accepted_out, workspace,
+                         stream=None) -> None:
+    """HHK Decaps with implicit rejection: Decrypt -> coins -> re-encrypt and compare -> K (R#20-R#23).
+    h, s, hpk, sigma, y_support are per KEY; key_index (None = identity) maps rows to keys."""
+    p = params(level)
+    B = _rows(u, 8 * p.u_stride, "u")
+    assert _rows(v, 8 * p.v_words, "v") == B and _rows(K_out, 64, "K_out") == B
+    _check(lib().hqc_kem_decaps_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk), _ptr(sigma),
+                                      _ptr(key_index), _ptr(y_support), _ptr(u), _ptr(v), _ptr(K_out),
+                                      _ptr(accepted_out), B, _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
 
 def hqc_decrypt_host_workspace_bytes(level: int, chunk: int) -> int:

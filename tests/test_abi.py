@@ -67,6 +67,16 @@ def test_host_validation(L):
     assert L.hqc_rm_decode_batch(ctypes.byref(p), a16, None, 4, None) == -2
     assert L.hqc_rs_decode_batch(ctypes.byref(p), a16, a8, 4, None) == -3
     assert L.hqc_status_str(-5) == b"CUDA launch error"
+    # KEM: workspace size is checked before anything is launched
+    ws = L.hqc_kem_workspace_bytes(ctypes.byref(p), 4)
+    assert ws >= 4 * (p.y_stride * 4 + p.k + 3 * p.e_stride * 4 + 1)
+    assert L.hqc_kem_workspace_bytes(ctypes.byref(bad), 4) == 0
+    args = [a16] * 10
+    assert L.hqc_kem_decaps_batch(ctypes.byref(p), *args[:5], *args[5:9], None, 4, a16, ws - 1, None) == -4
+    assert L.hqc_kem_decaps_batch(ctypes.byref(p), *args[:4], a8, *args[5:9], None, 4, a16, ws, None) == -3
+    assert L.hqc_kem_encaps_batch(ctypes.byref(p), a16, a16, a16, None, a16, a16, a16, None, 4, a16, ws, None) == -2
+    assert L.hqc_kem_encaps_batch(ctypes.byref(p), a16, a16, a16, None, a16, a16, a16, a16, 0, None, 0, None) == 0
+    assert L.hqc_kem_hpk_batch(ctypes.byref(p), a16, None, a16, 2, None) == -2
 
 
 def test_binding_refuses_cpu_tensors(L):
