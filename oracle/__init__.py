@@ -104,6 +104,7 @@ def lib():
             "orc_kem_hpk": (None, [P(_Params), c_p, c_p, c_p]),
             "orc_kem_coins": (None, [P(_Params), c_p, c_p, c_p, c_p, c_p]),
             "orc_kem_encaps": (None, [P(_Params), c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+            "orc_kem_keygen": (None, [P(_Params), c_p, c_p, c_p, c_p, c_p, c_p]),
             "orc_kem_decaps": (i32, [P(_Params), c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
             "orc_kem_decaps_batch": (None, [P(_Params), c_p, c_p, sz, c_p, c_p, c_p, c_p, sz, c_p, sz, c_p, sz, c_p,
                                             c_p, sz, i32]),
@@ -377,6 +378,19 @@ def kem_encaps(p: Params, h, s, hpk: bytes, m):
     K = np.zeros(64, np.uint8)
     lib().orc_kem_encaps(ctypes.byref(p._c()), _ptr(h), _ptr(s), _ptr(hp), _ptr(m), _ptr(u), _ptr(v), _ptr(K))
     return u, v, K.tobytes()
+
+
+def kem_keygen(p: Params, seed: bytes):
+    """KeyGen from a 32-byte seed (R#24): returns h (words), x, y (w positions), s (words), sigma (k bytes)."""
+    sd = np.frombuffer(bytes(seed), np.uint8).copy()
+    assert sd.size == 32
+    h = np.zeros(p.words, np.uint64)
+    s = np.zeros(p.words, np.uint64)
+    x = np.zeros(p.w, np.uint32)
+    y = np.zeros(p.w, np.uint32)
+    sigma = np.zeros(p.k, np.uint8)
+    lib().orc_kem_keygen(ctypes.byref(p._c()), _ptr(sd), _ptr(h), _ptr(x), _ptr(y), _ptr(s), _ptr(sigma))
+    return h, x, y, s, sigma
 
 
 def kem_decaps(p: Params, h, s, hpk: bytes, y, sigma, u, v):

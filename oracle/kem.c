@@ -9,6 +9,10 @@
  *        r2, e, each mapped to distinct positions by the fixed-weight sampler below;
  *   R#23 K = SHAKE256(m' || c || K, 64) when the re-encryption equals c, else SHAKE256(sigma || c || K, 64),
  *        with c = u bytes (ceil(n/8)) || v bytes (n1 n2 / 8).
+ *   R#24 KeyGen from a 32-byte seed: (seed_sk || seed_pk) = SHAKE256(seed || PRNG, 64);
+ *        h = SHAKE256(seed_pk || PRNG, ceil(n/8)) with bits >= n cleared ("sample_dense");
+ *        SHAKE256(seed_sk || PRNG, 8w + k) -> x = sample(words 0..w), y = sample(words w..2w),
+ *        sigma = bytes [8w, 8w + k); s = x + h*y (Alg. 3).
  * Fixed-weight sampler (R#22): p_i = i + floor(rand_i (n - i) / 2^32); then for i = w-1 down to 0,
  * p_i = i if p_i repeats a later entry. Every position is then distinct: p_i >= i for the
  * untouched entries and the replaced ones take the still-unused index i. */
@@ -99,4 +103,33 @@ int orc_kem_decaps(const orc_params *p, const uint64_t *h, const uint64_t *s, co
   kdf(p, eq ? m : sigma, u, v, K);
   free(m); free(r); free(u2); free(v2); free(um);
   return eq;
+}
+
+void orc_kem_keygen(const orc_params *p, const uint8_t seed[32], uint64_t *h, uint32_t *x, uint32_t *y,
+                    uint64_t *s, uint8_t *sigma) {
+  uint8_t in[33], seeds[64];
+  memcpy(in, seed, 32);
+  in[32] = 0x04; /* PRNG */
+  orc_shake256(in, 33, seeds, 64);
+  /* h from seed_pk */
+  const size_t nb = nbytes(p->n);
+  uint8_t *hb = (uint8_t *)calloc(8 * (size_t)p->words, 1);
+  memcpy(in, seeds + 32, 32);
+  orc_shake256(in, 33, hb, nb);
+  for (uint32_t i = 0; i < p->words; i++) {
+    uint64_t w = 0;
+    for (int b = 0; b < 8; b++) w |= (uint64_t)hb[8 * i + b] << (8 * b);
+    h[i] = w;
+  }
+  if (p->n % 64) h[p->words - 1] &= (~0ull) >> (64 - p->n % 64);
+  free(hb);
+  /* x, y, sigma from seed_sk */
+  uint8_t *r = (uint8_t *)malloc(8 * (size_t)p->w + p->k);
+  memcpy(in, seeds, 32);
+  orc_shake256(in, 33, r, 8 * (size_t)p->w + p->k);
+  orc_sample_fixed_weight(r, p->n, p->w, x);
+  orc_sample_fixed_weight(r + 4 * p->w, p->n, p->w, y);
+  memcpy(sigma, r + 8 * p->w, p->k);
+  free(r);
+  orc_keygen(p, h, x, y, s);
 }

@@ -106,6 +106,9 @@ void orc_kem_coins(const orc_params *p, const uint8_t hpk[32], const uint8_t *m,
 /* Encaps: c = Encrypt(pk, m; coins(m)), K = SHAKE256(m || c || 0x03, 64), c = u bytes || v bytes */
 void orc_kem_encaps(const orc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t hpk[32],
                     const uint8_t *m, uint64_t *u, uint64_t *v, uint8_t K[64]);
+/* KeyGen from a 32-byte seed (R#24): h (p->words, bits >= n zero), x, y (w positions each), s, sigma (k bytes) */
+void orc_kem_keygen(const orc_params *p, const uint8_t seed[32], uint64_t *h, uint32_t *x, uint32_t *y,
+                    uint64_t *s, uint8_t *sigma);
 /* Decaps: m' = Decrypt; c' = Encrypt(pk, m'; coins(m')); K = SHAKE256((c' == c ? m' : sigma) || c || 0x03, 64).
    Returns 1 if the ciphertext was accepted (c' == c). */
 int orc_kem_decaps(const orc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t hpk[32],

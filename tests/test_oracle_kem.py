@@ -122,3 +122,44 @@ def test_decaps_batch_matches_single():
         Ki, oki = oracle.kem_decaps(p, h[kk], s[kk], hpk[kk].tobytes(), y[kk], sigma[kk], U[i], V[i])
         assert K[i].tobytes() == Ki and acc[i] == oki
     assert acc.tolist() == [1, 1, 0, 1, 1]
+
+
+def _words_le(b: bytes, nwords: int) -> np.ndarray:
+    return np.frombuffer(b + bytes(8 * nwords - len(b)), "<u8").astype(np.uint64)
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_keygen_from_seed_definition(level):
+    """R#24 recomputed from its definition with hashlib; s = x + h*y through the (schoolbook-pinned)
+    keygen product; sample_dense masks bits >= n and has weight ~ n/2."""
+    p = oracle.params(level)
+    nb = (p.n + 7) // 8
+    for t in range(3):
+        seed = bytes(np.random.default_rng(1000 * level + t).integers(0, 256, 32, dtype=np.uint8))
+        h, x, y, s, sigma = oracle.kem_keygen(p, seed)
+        seeds = hashlib.shake_256(seed + b"\x04").digest(64)
+        hb = bytearray(hashlib.shake_256(seeds[32:] + b"\x04").digest(nb))
+        if p.n % 8:
+            hb[-1] &= (1 << (p.n % 8)) - 1
+        assert (h == _words_le(bytes(hb), p.words)).all()
+        r = hashlib.shake_256(seeds[:32] + b"\x04").digest(8 * p.w + p.k)
+        assert (x == oracle.sample_fixed_weight(r[: 4 * p.w], p.n, p.w)).all()
+        assert (y == oracle.sample_fixed_weight(r[4 * p.w: 8 * p.w], p.n, p.w)).all()
+        assert sigma.tobytes() == r[8 * p.w:]
+        assert (s == oracle.keygen(p, h, x, y)).all()
+        assert len(set(x.tolist())) == p.w and len(set(y.tolist())) == p.w
+        wt = sum(bin(int(v)).count("1") for v in h)
+        assert abs(wt - p.n / 2) < 4 * (p.n / 4) ** 0.5
+        again = oracle.kem_keygen(p, seed)
+        assert all((a == b).all() for a, b in zip(again, (h, x, y, s, sigma)))
+
+
+@pytest.mark.parametrize("level", [1, 5])
+def test_kem_round_trip_with_seeded_keys(level):
+    p = oracle.params(level)
+    h, x, y, s, sigma = oracle.kem_keygen(p, bytes(range(32)))
+    hpk = oracle.kem_hpk(p, h, s)
+    m = np.arange(p.k, dtype=np.uint8)
+    u, v, K = oracle.kem_encaps(p, h, s, hpk, m)
+    K2, ok = oracle.kem_decaps(p, h, s, hpk, y, sigma, u, v)
+    assert ok and K2 == K
