@@ -156,6 +156,18 @@ int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
  * supports and the comparison flags and may be reused once the stream has passed the call.
  * Encaps takes m from the caller (the message draw is the caller's randomness).
  * ------------------------------------------------------------------------------------------- */
+/* KeyGen from seeds (Alg. 3; reading R#24), one key per seed:
+ *   (seed_sk || seed_pk) = SHAKE256(seed || 0x04, 64)
+ *   h     = SHAKE256(seed_pk || 0x04, ceil(n/8)) as LE bits, bits >= n cleared
+ *   SHAKE256(seed_sk || 0x04, 8w + k) -> x = sample(u32 words 0..w), y = sample(words w..2w) with the
+ *           fixed-weight sampler of R#22, sigma = bytes [8w, 8w + k)
+ *   s     = x + h*y (the product of hqc_keygen_batch); hpk = H_pk (as hqc_kem_hpk_batch) if hpk_out != NULL
+ * seeds [nkeys][32] uint8; h_out, s_out [nkeys][u_stride] uint64 (padding words zero); x_out, y_out
+ * [nkeys][y_stride] uint32 (entries >= w zero; positions distinct, in [0, n), unsorted); sigma_out
+ * [nkeys][k]; hpk_out [nkeys][32] (nullable). All device pointers, 16-byte aligned; nkeys = 0 is a no-op. */
+int hqc_kem_keygen_batch(const hqc_params *p, const uint8_t *seeds, uint64_t *h_out, uint32_t *x_out,
+                         uint32_t *y_out, uint64_t *s_out, uint8_t *sigma_out, uint8_t *hpk_out, size_t nkeys,
+                         void *stream);
 size_t hqc_kem_workspace_bytes(const hqc_params *p, size_t batch);
 int hqc_kem_hpk_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, uint8_t *hpk_out,
                       size_t nkeys, void *stream);

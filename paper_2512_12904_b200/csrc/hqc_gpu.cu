@@ -213,6 +213,19 @@ extern "C" int hqc_kem_hpk_batch(const hqc_params *p, const uint64_t *h, const u
   HQC_DISPATCH(p, kem_hpk, h, s, hpk_out, nkeys, (cudaStream_t)stream);
 }
 
+extern "C" int hqc_kem_keygen_batch(const hqc_params *p, const uint8_t *seeds, uint64_t *h_out, uint32_t *x_out,
+                                    uint32_t *y_out, uint64_t *s_out, uint8_t *sigma_out, uint8_t *hpk_out,
+                                    size_t nkeys, void *stream) {
+  int st = check_level(p);
+  if (st) return st;
+  if (nkeys == 0) return HQC_OK;
+  if (nkeys > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(seeds); HQC_CHECK_PTR(h_out); HQC_CHECK_PTR(x_out); HQC_CHECK_PTR(y_out); HQC_CHECK_PTR(s_out);
+  HQC_CHECK_PTR(sigma_out);
+  if (hpk_out && misaligned(hpk_out)) return HQC_ERR_ALIGN;
+  HQC_DISPATCH(p, kem_keygen, seeds, h_out, x_out, y_out, s_out, sigma_out, hpk_out, nkeys, (cudaStream_t)stream);
+}
+
 extern "C" int hqc_kem_encaps_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s, const uint8_t *hpk,
                                     const uint32_t *key_index, const uint8_t *m, uint64_t *u_out, uint64_t *v_out,
                                     uint8_t *K_out, size_t batch, void *d_work, size_t work_bytes, void *stream) {

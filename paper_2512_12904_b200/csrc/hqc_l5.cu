@@ -25,6 +25,10 @@ int encrypt_l5(const uint64_t *h, const uint64_t *s, const uint32_t *key, const 
 }
 int shape_l5(size_t batch, int *grid, int *wpc) { return shape_impl<PL>(batch, grid, wpc); }
 size_t kem_ws_l5(size_t batch) { return kem_ws_bytes<PL>(batch); }
+int kem_keygen_l5(const uint8_t *seeds, uint64_t *h, uint32_t *x, uint32_t *y, uint64_t *s, uint8_t *sigma,
+                   uint8_t *hpk, size_t nkeys, cudaStream_t st) {
+  return launch_kem_keygen<PL>(seeds, h, x, y, s, sigma, hpk, nkeys, st);
+}
 int kem_hpk_l5(const uint64_t *h, const uint64_t *s, uint8_t *hpk, size_t nkeys, cudaStream_t st) {
   return launch_kem_hpk<PL>(h, s, hpk, nkeys, st);
 }

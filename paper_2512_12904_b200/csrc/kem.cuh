@@ -194,6 +194,97 @@ __global__ void __launch_bounds__(128) k_kem_kdf(const uint8_t *__restrict__ m, 
                       (uint32_t)(A[2 * i + 1] >> 32));
 }
 
+// ---- KeyGen from a 32-byte seed (lane per key; R#24, Alg. 3):
+//   (seed_sk || seed_pk) = SHAKE256(seed || PRNG, 64)
+//   h = SHAKE256(seed_pk || PRNG, ceil(n/8)), bits >= n cleared          ("sample_dense")
+//   SHAKE256(seed_sk || PRNG, 8w + k) -> x = sample(u32 words 0..w), y = sample(words w..2w),
+//                                        sigma = bytes [8w, 8w + k)
+// The product s = x + h*y is the keygen kernel's (k_keygen) and runs afterwards on the same stream.
+// The sampler's duplicate scan runs in the lane's own output row (L1-resident; keys are few).
+template <class P>
+__global__ void __launch_bounds__(128) k_kem_keygen_seed(const uint8_t *__restrict__ seeds, uint64_t *__restrict__ h,
+                                                         uint32_t *__restrict__ x, uint32_t *__restrict__ y,
+                                                         uint8_t *__restrict__ sigma, size_t nkeys) {
+  using KS = KemShape<P>;
+  const size_t key = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= nkeys) return;
+  uint64_t A[25], sd[8];
+  {
+    CatReader<4, 0, 0, 0x04> rd;
+    const uint64_t *sp = reinterpret_cast<const uint64_t *>(seeds + key * 32);
+#pragma unroll
+    for (int i = 0; i < 4; i++) rd.f[i] = sp[i];
+    rd.a = rd.b = nullptr;
+    shake256_absorb<decltype(rd)::LEN>(A, rd);
+#pragma unroll
+    for (int i = 0; i < 8; i++) sd[i] = A[i];
+  }
+  {  // h from seed_pk: ceil(n/8) bytes = words [0, U_WORDS), the last one masked to bit n
+    CatReader<4, 0, 0, 0x04> rd;
+#pragma unroll
+    for (int i = 0; i < 4; i++) rd.f[i] = sd[4 + i];
+    rd.a = rd.b = nullptr;
+    shake256_absorb<decltype(rd)::LEN>(A, rd);
+    uint64_t *hr = h + key * P::U_STRIDE;
+    constexpr uint32_t NBLK = (P::U_WORDS + SHAKE256_RATE_W - 1) / SHAKE256_RATE_W;
+    constexpr uint64_t LAST = (P::N % 64) ? (~0ull >> (64 - P::N % 64)) : ~0ull;
+#pragma unroll 1
+    for (uint32_t blk = 0; blk < NBLK; blk++) {
+      if (blk) keccak_f1600(A);
+#pragma unroll
+      for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) {
+        const uint32_t t = blk * SHAKE256_RATE_W + i;
+        if (t < P::U_WORDS) hr[t] = t == P::U_WORDS - 1 ? (A[i] & LAST) : A[i];
+      }
+    }
+#pragma unroll
+    for (uint32_t t = P::U_WORDS; t < P::U_STRIDE; t++) hr[t] = 0;
+  }
+  uint32_t *xr = x + key * P::Y_STRIDE, *yr = y + key * P::Y_STRIDE;
+  {  // x, y positions (before deduplication) and sigma from seed_sk
+    CatReader<4, 0, 0, 0x04> rd;
+#pragma unroll
+    for (int i = 0; i < 4; i++) rd.f[i] = sd[i];
+    rd.a = rd.b = nullptr;
+    shake256_absorb<decltype(rd)::LEN>(A, rd);
+    constexpr uint32_t NW = P::W + KS::KW;  // 64-bit output words: 2w u32 sampler words, then sigma
+    constexpr uint32_t NBLK = (NW + SHAKE256_RATE_W - 1) / SHAKE256_RATE_W;
+    uint64_t *sg = reinterpret_cast<uint64_t *>(sigma + key * P::K);
+#pragma unroll 1
+    for (uint32_t blk = 0; blk < NBLK; blk++) {
+      if (blk) keccak_f1600(A);
+#pragma unroll
+      for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) {
+        const uint32_t g = blk * SHAKE256_RATE_W + i;
+        if (g < P::W) {
+#pragma unroll
+          for (uint32_t hf = 0; hf < 2; hf++) {
+            const uint32_t t = 2 * g + hf, idx = t % P::W;
+            const uint32_t rnd = (uint32_t)(A[i] >> (32 * hf));
+            (t < P::W ? xr : yr)[idx] = idx + __umulhi(rnd, P::N - idx);
+          }
+        } else if (g < NW) {
+          sg[g - P::W] = A[i];
+        }
+      }
+    }
+  }
+#pragma unroll 1
+  for (uint32_t which = 0; which < 2; which++) {  // R#22 deduplication, fixed w(w-1)/2 compares
+    uint32_t *row = which ? yr : xr;
+#pragma unroll 1
+    for (int i = (int)P::W - 1; i >= 0; i--) {
+      const uint32_t pi = row[i];
+      uint32_t dup = 0;
+#pragma unroll 4
+      for (uint32_t j = i + 1; j < P::W; j++) dup |= (uint32_t)(row[j] == pi);
+      row[i] = dup ? (uint32_t)i : pi;
+    }
+#pragma unroll
+    for (uint32_t t = P::W; t < P::Y_STRIDE; t++) row[t] = 0;
+  }
+}
+
 // rows dst[b] = src[key_index[b]] (16-byte chunks)
 static __global__ void __launch_bounds__(256) k_gather_rows(const uint4 *__restrict__ src, const uint32_t *__restrict__ key_index,
                                                      uint4 *__restrict__ dst, uint32_t row_chunks, size_t batch) {
@@ -240,6 +331,16 @@ static int launch_kem_coins(const uint8_t *hpk, const uint32_t *key, const uint8
   k_kem_coins<P, KEM_COIN_WARPS><<<(unsigned)((batch + per - 1) / per), 32 * KEM_COIN_WARPS, smem, st>>>(
       hpk, key, m, r1, r2, e, batch);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_kem_keygen(const uint8_t *seeds, uint64_t *h, uint32_t *x, uint32_t *y, uint64_t *s, uint8_t *sigma,
+                             uint8_t *hpk, size_t nkeys, cudaStream_t st) {
+  k_kem_keygen_seed<P><<<(unsigned)((nkeys + 127) / 128), 128, 0, st>>>(seeds, h, x, y, sigma, nkeys);
+  if (cudaGetLastError() != cudaSuccess) return HQC_ERR_CUDA;
+  int rc = launch_keygen<P>(h, x, y, s, nkeys, st);
+  if (rc || !hpk) return rc;
+  return launch_kem_hpk<P>(h, s, hpk, nkeys, st);
 }
 
 template <class P> static int encrypt_grid(size_t batch, size_t *grid) {

@@ -19,6 +19,8 @@
                    size_t batch, cudaStream_t st);                                                              \
   int shape_l##L(size_t batch, int *grid, int *wpc);                                                            \
   size_t kem_ws_l##L(size_t batch);                                                                             \
+  int kem_keygen_l##L(const uint8_t *seeds, uint64_t *h, uint32_t *x, uint32_t *y, uint64_t *s, uint8_t *sigma,    \
+                      uint8_t *hpk, size_t nkeys, cudaStream_t st);                                             \
   int kem_hpk_l##L(const uint64_t *h, const uint64_t *s, uint8_t *hpk, size_t nkeys, cudaStream_t st);          \
   int kem_encaps_l##L(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint32_t *key,            \
                       const uint8_t *m, uint64_t *u, uint64_t *v, uint8_t *K, size_t batch, void *ws,           \

@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
             "hqc_keygen_batch": [P, vp, vp, vp, vp, sz, vp],
             "hqc_encrypt_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hqc_kem_hpk_batch": [P, vp, vp, vp, sz, vp],
+            "hqc_kem_keygen_batch": [P, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hqc_kem_encaps_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, sz, vp],
             "hqc_kem_decaps_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, sz, vp],
         }
@@ -221,6 +222,19 @@ def hqc_kem_hpk_batch(level: int, h, s, hpk_out, stream=None) -> None:
     K = _rows(h, 8 * p.u_stride, "h")
     assert _rows(s, 8 * p.u_stride, "s") == K and _rows(hpk_out, 32, "hpk_out") == K
     _check(lib().hqc_kem_hpk_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk_out), K, _stream(stream)))
+
+
+def hqc_kem_keygen_batch(level: int, seeds, h_out, x_out, y_out, s_out, sigma_out, hpk_out=None, stream=None) -> None:
+    """KeyGen from 32-byte seeds (R#24): h, x, y, sigma by SHAKE256 expansion, s = x + h*y, H_pk."""
+    p = params(level)
+    K = _rows(seeds, 32, "seeds")
+    assert _rows(h_out, 8 * p.u_stride, "h_out") == K and _rows(s_out, 8 * p.u_stride, "s_out") == K
+    assert _rows(x_out, 4 * p.y_stride, "x_out") == K and _rows(y_out, 4 * p.y_stride, "y_out") == K
+    assert _rows(sigma_out, p.k, "sigma_out") == K
+    if hpk_out is not None:
+        assert _rows(hpk_out, 32, "hpk_out") == K
+    _check(lib().hqc_kem_keygen_batch(ctypes.byref(_cp(level)), _ptr(seeds), _ptr(h_out), _ptr(x_out), _ptr(y_out),
+                                      _ptr(s_out), _ptr(sigma_out), _ptr(hpk_out), K, _stream(stream)))
 
 
 def hqc_kem_encaps_batch(level: int, h, s, hpk, key_index, m, u_out, v_out, K_out, workspace, stream=None) -> None:

@@ -170,3 +170,69 @@ def test_decaps_without_key_index():
     torch.cuda.synchronize()
     assert acc.cpu().numpy()[:B].tolist() == accref.tolist() == [1, 1, 0, 1, 1]
     assert (K.cpu().numpy()[: B * 64].reshape(B, 64) == Kref).all()
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_keygen_from_seed_matches_oracle(level):
+    """hqc_kem_keygen_batch (R#24) against oracle.kem_keygen (pinned against hashlib and the schoolbook-
+    pinned keygen product in tests/test_oracle_kem.py) and oracle.kem_hpk, over a ragged 128-lane tail."""
+    p, g = oracle.params(level), hqc.params(level)
+    nk = 133
+    seeds = gen.rand_bytes(SEED, gen.TAG_TEST, 7000 + level, nk, 32)
+    h, x, y, s = empty(nk * g.u_stride * 8), empty(nk * g.y_stride * 4), empty(nk * g.y_stride * 4), \
+        empty(nk * g.u_stride * 8)
+    sigma, hpk = empty(nk * p.k), empty(nk * 32)
+    for t in (h, x, y, s):
+        t.fill_(0xA5)  # padding must be written, not inherited
+    hqc.hqc_kem_keygen_batch(level, dev(seeds), h, x, y, s, sigma, hpk)
+    torch.cuda.synchronize()
+    gh, gs = host(h, np.uint64, g.u_stride), host(s, np.uint64, g.u_stride)
+    gx, gy = host(x, np.uint32, g.y_stride), host(y, np.uint32, g.y_stride)
+    gsig, ghpk = sigma.cpu().numpy()[: nk * p.k].reshape(nk, p.k), hpk.cpu().numpy()[: nk * 32].reshape(nk, 32)
+    for i in list(range(0, nk, 7)) + [nk - 1]:
+        rh, rx, ry, rs, rsig = oracle.kem_keygen(p, seeds[i].tobytes())
+        assert (gh[i, : p.words] == rh).all() and (gh[i, p.words:] == 0).all(), i
+        assert (gs[i, : p.words] == rs).all() and (gs[i, p.words:] == 0).all(), i
+        assert (gx[i, : p.w] == rx).all() and (gx[i, p.w:] == 0).all(), i
+        assert (gy[i, : p.w] == ry).all() and (gy[i, p.w:] == 0).all(), i
+        assert (gsig[i] == rsig).all(), i
+        assert ghpk[i].tobytes() == oracle.kem_hpk(p, gh[i], gs[i]), i
+    # properties on every key: distinct positions < n
+    for arr in (gx, gy):
+        a = arr[:, : p.w]
+        assert (a < p.n).all()
+        srt = np.sort(a, axis=1)
+        assert (np.diff(srt.astype(np.int64), axis=1) > 0).all()
+
+
+def test_kem_round_trip_with_seeded_gpu_keys():
+    """Seeds -> GPU KeyGen -> GPU Encaps -> GPU Decaps: all accepted, equal keys; one tampered row rejected
+    with the oracle's implicit-rejection key."""
+    level, nk, B = 3, 4, 130
+    p, g = oracle.params(level), hqc.params(level)
+    seeds = gen.rand_bytes(SEED, gen.TAG_TEST, 7100, nk, 32)
+    h, x, y, s = empty(nk * g.u_stride * 8), empty(nk * g.y_stride * 4), empty(nk * g.y_stride * 4), \
+        empty(nk * g.u_stride * 8)
+    sigma, hpk = empty(nk * p.k), empty(nk * 32)
+    hqc.hqc_kem_keygen_batch(level, dev(seeds), h, x, y, s, sigma, hpk)
+    key = (np.arange(B) % nk).astype(np.uint32)
+    m = gen.rand_bytes(SEED, gen.TAG_TEST, 7200, B, p.k)
+    u, v, K1, K2, acc = empty(B * g.u_stride * 8), empty(B * g.v_words * 8), empty(B * 64), empty(B * 64), empty(B)
+    ws = empty(hqc.hqc_kem_workspace_bytes(level, B))
+    dkey = dev(key)
+    hqc.hqc_kem_encaps_batch(level, h, s, hpk, dkey, dev(m), u, v, K1, ws)
+    v64 = v.view(torch.int64)
+    v64[5 * g.v_words + 3] ^= 1 << 20
+    hqc.hqc_kem_decaps_batch(level, h, s, hpk, sigma, dkey, y, u, v, K2, acc, ws)
+    torch.cuda.synchronize()
+    a = acc.cpu().numpy()[:B]
+    assert a[5] == 0 and a.sum() == B - 1
+    k1, k2 = K1.cpu().numpy()[: B * 64].reshape(B, 64), K2.cpu().numpy()[: B * 64].reshape(B, 64)
+    ok = np.arange(B) != 5
+    assert (k1[ok] == k2[ok]).all() and (k1[5] != k2[5]).any()
+    rh, rx, ry, rs, rsig = oracle.kem_keygen(p, seeds[key[5]].tobytes())
+    U = host(u, np.uint64, g.u_stride)[5:6]
+    V = host(v, np.uint64, g.v_words)[5:6]
+    Kref, accref = oracle.kem_decaps_batch(p, rh[None], rs[None], np.frombuffer(oracle.kem_hpk(p, rh, rs), np.uint8)[None],
+                                           rsig[None], np.zeros(1, np.int64), ry[None], U, V)
+    assert accref[0] == 0 and (k2[5] == Kref[0]).all()
