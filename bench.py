@@ -40,6 +40,20 @@ def algorithmic_ops(p) -> dict:
                 abi_bytes=8 * p.u_stride + 8 * p.v_words + 4 * p.y_stride + p.k)
 
 
+def ncu_traffic(level: int, batch: int):
+    """DRAM bytes (read + write) per launch of the fused kernel from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, scripts/ncu_traffic.py), scaled from its batch to this launch's batch."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)[str(level)]
+    except (OSError, KeyError, ValueError):
+        return None, None
+    src = f"profiles/ncu_traffic.json: {t['report']} (batch {t['batch']}), dram__bytes_read.sum + dram__bytes_write.sum"
+    if batch != t["batch"]:
+        src += f", scaled per decryption ({t['bytes_per_decryption']:.0f} B) to batch {batch}"
+    return t["bytes_per_decryption"] * batch, src
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -423,8 +437,10 @@ def main():
     kernel_s = ms / 1e3 / args.steps
     achieved = ops["total"] * B / kernel_s / 1e12
     peak = 64 * sms * sm_max * 1e6 / 1e12  # ALU pipe: 64 lanes/clk/SM (K7-measured 63.7)
+    traffic, traffic_src = ncu_traffic(args.level, B)
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tintop/s", "frac": achieved / peak,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": f"64 ALU lanes/clk/SM x {sms} SMs x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "ops_per_decryption": ops["total"],
             "frac_at_measured_clock": (achieved / (64 * sms * c["sm_mhz"] * 1e6 / 1e12)) if c["sm_mhz"] else None,
@@ -442,7 +458,8 @@ def main():
            "config": {"workload": WORKLOAD[args.level], "level": args.level, "batch_per_gpu": B,
                       "global_batch": world * B, "parallelism": f"dp{world}",
                       "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB/GPU > 126 MB L2, no flush needed",
-                      "launch": {"kernel": "k_decrypt (fused)", "grid": gw[0], "warps_per_cta": gw[1]}},
+                      "launch": {"kernel": "k_decrypt (fused, warp pair)" if gw[1] == 2 else "k_decrypt_w1 (fused, one warp)",
+                                 "grid": gw[0], "warps_per_cta": gw[1]}},
            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
            "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"],
                       "samples": c["samples"], "source": "NVML, 2 ms period, timed region only"}}
