@@ -107,6 +107,17 @@ int hqc_rs_decode_batch(const hqc_params *p, const uint8_t *sym, uint8_t *m_out,
 int hqc_rs_decode_batch_ex(const hqc_params *p, const uint8_t *sym, uint8_t *m_out,
                            uint8_t *ok_out, size_t batch, void *stream);
 
+/* Step a6 alone (§8(f) row 4): syn_out[b][i-1] = S_i = sum_{j<n1} sym[b][j] alpha^{i j},
+ * i = 1..2delta (readings R#4, R#5). sym [batch][n1] uint8 -> syn_out [batch][2 delta] uint8.
+ * method selects how the GF(2^8) products are formed; all give the same bytes:
+ *   0 = GF(2)-linear map with constant-bank tables (the fused kernel's method),
+ *   1 = the paper's nibble-sliced tables (two 16-entry lookups per byte, "hi XOR lo") in shared
+ *       memory, 4 syndromes per 32-bit entry,
+ *   2 = log/antilog tables in shared memory.
+ * An unknown method returns HQC_ERR_SIZE. */
+int hqc_rs_syndromes_batch(const hqc_params *p, const uint8_t *sym, uint8_t *syn_out, size_t batch, int method,
+                           void *stream);
+
 /* Helpers for tests and the bench.
  * hqc_count_mismatch: *d_count += #{b : m_out[b] != m_ref[b]} (d_count: one device uint64, the
  *   caller zeroes it). hqc_validate_support: *d_bad += #{rows with an entry >= n or a repeated

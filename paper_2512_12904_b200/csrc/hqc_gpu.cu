@@ -138,6 +138,17 @@ extern "C" int hqc_rs_decode_batch(const hqc_params *p, const uint8_t *sym, uint
   return hqc_rs_decode_batch_ex(p, sym, m, nullptr, batch, stream);
 }
 
+extern "C" int hqc_rs_syndromes_batch(const hqc_params *p, const uint8_t *sym, uint8_t *syn_out, size_t batch,
+                                      int method, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (method < 0 || method > 2) return HQC_ERR_SIZE;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  HQC_CHECK_PTR(sym); HQC_CHECK_PTR(syn_out);
+  HQC_DISPATCH(p, syndromes, sym, syn_out, batch, method, (cudaStream_t)stream);
+}
+
 extern "C" int hqc_count_mismatch(const hqc_params *p, const uint8_t *a, const uint8_t *b, size_t batch,
                                   unsigned long long *count, void *stream) {
   int s = check_level(p);

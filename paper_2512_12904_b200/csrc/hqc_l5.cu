@@ -2,6 +2,7 @@
 #define HQC_THIS_LEVEL 5
 #include "kernels.cuh"
 #include "kem.cuh"
+#include "syndromes.cuh"
 #include "launchers.h"
 
 namespace hqc {
@@ -22,6 +23,9 @@ int keygen_l5(const uint64_t *h, const uint32_t *x, const uint32_t *y, uint64_t 
 int encrypt_l5(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m, const uint32_t *r1,
                 const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v, size_t batch, cudaStream_t st) {
   return launch_encrypt<PL>(h, s, key, m, r1, r2, e, u, v, batch, st);
+}
+int syndromes_l5(const uint8_t *sym, uint8_t *syn, size_t batch, int method, cudaStream_t st) {
+  return launch_syndromes<PL>(sym, syn, batch, method, st);
 }
 int shape_l5(size_t batch, int *grid, int *wpc) { return shape_impl<PL>(batch, grid, wpc); }
 size_t kem_ws_l5(size_t batch) { return kem_ws_bytes<PL>(batch); }

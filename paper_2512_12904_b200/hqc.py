@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
             "hqc_rm_decode_batch": [P, vp, vp, sz, vp],
             "hqc_rs_decode_batch": [P, vp, vp, sz, vp],
             "hqc_rs_decode_batch_ex": [P, vp, vp, vp, sz, vp],
+            "hqc_rs_syndromes_batch": [P, vp, vp, sz, i32, vp],
             "hqc_count_mismatch": [P, vp, vp, sz, vp, vp],
             "hqc_validate_support": [P, vp, sz, vp, vp],
             "hqc_decrypt_launch_shape": [P, sz, ctypes.POINTER(i32), ctypes.POINTER(i32)],
@@ -164,6 +165,18 @@ def hqc_rs_decode_batch(level: int, sym, m_out, ok_out=None, stream=None) -> Non
     B = _rows(sym, p.n1, "sym")
     assert _rows(m_out, p.k, "m_out") == B
     _check(lib().hqc_rs_decode_batch_ex(ctypes.byref(_cp(level)), _ptr(sym), _ptr(m_out), _ptr(ok_out), B,
+                                        _stream(stream)))
+
+
+SYN_METHODS = {"linear": 0, "nibble": 1, "logexp": 2}
+
+
+def hqc_rs_syndromes_batch(level: int, sym, syn_out, method: str = "linear", stream=None) -> None:
+    """S_1..S_2delta of each received word (step a6); method: linear | nibble | logexp."""
+    p = params(level)
+    B = _rows(sym, p.n1, "sym")
+    assert _rows(syn_out, 2 * p.delta, "syn_out") == B
+    _check(lib().hqc_rs_syndromes_batch(ctypes.byref(_cp(level)), _ptr(sym), _ptr(syn_out), B, SYN_METHODS[method],
                                         _stream(stream)))
 
 

@@ -54,6 +54,9 @@ def test_host_validation(L):
     L.hqc_get_params(1, ctypes.byref(p))
     a16 = ctypes.c_void_p(0x1000)
     a8 = ctypes.c_void_p(0x1008)
+    # unknown syndrome method
+    assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 3, None) == -4
+    assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 1, None) == 0
     # batch 0 is a no-op even with NULL pointers
     assert L.hqc_decrypt_batch(ctypes.byref(p), None, None, None, None, 0, None) == 0
     assert L.hqc_decrypt_batch(ctypes.byref(p), None, a16, a16, a16, 4, None) == -2

@@ -101,3 +101,52 @@ def test_gpu_encrypt_decrypt_round_trip_full_size(level, B):
         k = key[i]
         ou, ov = oracle.encrypt(p, h[k], sh_np[k], m[i], r1[i], r2[i], e[i])
         assert (gu[i, : p.words] == ou).all() and (gv[i] == ov).all()
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_scaling_config_full_size(level):
+    """BASELINE configs[4]: 4,194,304 ciphertexts per level in ONE launch (the G = 1 shard), built on the
+    device exactly as bench.py builds them (generator draws -> GPU keygen + encrypt, one key per 256).
+    Every row must decrypt to its generator message (on-device mismatch count); a sample of rows is
+    re-encrypted and decrypted by the oracle; and the rows of shard 5 of G = 8 regenerated on their own
+    are byte-identical to the same rows of the G = 1 workload (per-index seeding)."""
+    import bench
+
+    B = 4_194_304
+    g = hqc.params(level)
+    p = oracle.params(level)
+    du, dv, dy, dref = bench.make_valid_workload(level, 0, B, g, DEV)
+    mo = torch.empty(B * g.k, dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch(level, du, dv, dy, mo)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    hqc.hqc_count_mismatch(level, mo, dref, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    U = du.view(B, -1)
+    V = dv.view(B, -1)
+    Y = dy.view(B, -1)
+    M = mo.view(B, -1)
+    idx = np.sort(np.random.default_rng(level).choice(B, 24, replace=False))
+    ti = torch.from_numpy(idx).to(DEV)
+    su = U[ti].cpu().numpy().view(np.uint64)
+    sv = V[ti].cpu().numpy().view(np.uint64)
+    sy = Y[ti].cpu().numpy().view(np.uint32)
+    sm = M[ti].cpu().numpy()
+    assert (oracle.decrypt_batch(p, su, sv, sy) == sm).all()
+    sh = shape_for(level)
+    seed = bench.CONFIG_SEED[level]
+    for i in idx[:4]:
+        i = int(i)
+        key = i // 256
+        h, x, y = gen.key_draws(seed, sh, key, 1)
+        s = oracle.keygen(p, h[0], x[0], y[0])
+        m, r1, r2, e = gen.ct_draws(seed, sh, i, 1)
+        u, v = oracle.encrypt_batch(p, h, s[None], np.zeros(1, np.int64), m, r1, r2, e)
+        j = int(np.nonzero(idx == i)[0][0])
+        assert (su[j, : p.words] == u[0]).all() and (sv[j] == v[0]).all()
+    r0 = 5 * B // 8 + 1000  # inside shard 5 of G = 8, not on a key boundary
+    eu, ev, ey, em = bench.make_valid_workload(level, r0, 40, g, DEV)
+    assert torch.equal(eu.view(40, -1), U[r0:r0 + 40]) and torch.equal(ev.view(40, -1), V[r0:r0 + 40])
+    assert torch.equal(ey.view(40, -1), Y[r0:r0 + 40]) and torch.equal(em.view(40, -1), dref.view(B, -1)[r0:r0 + 40])
+    del du, dv, dy, dref, mo, U, V, Y, M
+    torch.cuda.empty_cache()

@@ -178,6 +178,29 @@ def test_stage3_rs(level):
     assert ok[kinds <= 2].all() and not ok[kinds == 4].any()
 
 
+@pytest.mark.parametrize("level", LEVELS)
+@pytest.mark.parametrize("method", ["linear", "nibble", "logexp"])
+def test_stage_a6_syndromes_all_methods(level, method):
+    """Step a6 alone (hqc_rs_syndromes_batch), each of the three GF-product methods, against the oracle's
+    Horner evaluation S_i = r(alpha^i) (oracle/rs.c), on random words, words with zero symbols, codewords
+    (all-zero syndromes) and the all-zero / all-0xFF words; 197 rows = 6 warps and a ragged tail."""
+    p = oracle.params(level)
+    rng = np.random.default_rng(300 + level)
+    B = 197
+    sym = rng.integers(0, 256, (B, p.n1)).astype(np.uint8)
+    sym[1::7] &= rng.integers(0, 2, (len(sym[1::7]), p.n1)).astype(np.uint8) * 0xFF  # many zero symbols
+    for i in range(2, B, 11):
+        sym[i] = oracle.rs_encode(rng.integers(0, 256, p.k).astype(np.uint8), p.n1, p.k)
+    sym[3] = 0
+    sym[4] = 0xFF
+    ref = np.stack([oracle.rs_syndromes(r, p.n1, p.delta) for r in sym])
+    assert not ref[2::11].any()
+    out = torch.empty(B * 2 * p.delta, dtype=torch.uint8, device=DEV)
+    hqc.hqc_rs_syndromes_batch(level, to_dev(sym), out, method)
+    torch.cuda.synchronize()
+    assert (from_dev(out, np.uint8, 2 * p.delta) == ref).all()
+
+
 # ---------------------------------------------------------------- API behaviour
 def test_batch_zero_and_errors():
     p = hqc.params(1)
