@@ -92,7 +92,7 @@ __device__ __forceinline__ void copy_s2g(void *dst, const uint32_t *src, uint32_
 
 // One warp: out (NOUT words in smem, aliasing E) = dense (staged in su) * support (staged in ssup)
 template <class P, class S>
-__device__ __forceinline__ void warp_product(const uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
+__device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
                                              int lane) {
   s1_stage_d<P, S>(ssup, dsm, lane);
   s1_build_E<P, S>(su, E, lane);

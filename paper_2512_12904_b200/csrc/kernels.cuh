@@ -48,7 +48,10 @@ template <class P> struct WarpSmem {
   static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
   static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16);
   static constexpr uint32_t D_BYTES = round_up(DecShape<P>::WPAD * 4, 16);
-  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 32, 16);
+  // symbol rows [j][slot] with a 36-byte pitch: 9 words per row (odd), so the stage-2 byte stores of one
+  // slot by the lanes j = 0..31 fall in 32 distinct banks (a 32-byte pitch made them 8-way conflicts)
+  static constexpr uint32_t SYM_PITCH = 36;
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
   static constexpr uint32_t BAR_BYTES = 16;
   static constexpr uint32_t S1_BYTES = E_BYTES + STG_BYTES + D_BYTES + BAR_BYTES;  // stage-1 kernel
   static constexpr uint32_t BYTES = S1_BYTES + SYM_BYTES;                          // fused kernel
@@ -225,15 +228,15 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
           const uint4 x = src[c];
           X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
         }
-        sb[j * 32 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+        sb[j * WarpSmem<P>::SYM_PITCH + s] = (uint8_t)rm_decode_block<P::MULT>(X);
       }
       __syncwarp();
     }
     for (uint32_t s = rows; s < 32; s++)
-      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * 32 + s] = 0;
+      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * WarpSmem<P>::SYM_PITCH + s] = 0;
     __syncwarp();
     const bool act = (uint32_t)lane < rows;
-    auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
+    auto sym_at = [&](int j) -> uint32_t { return sb[j * WarpSmem<P>::SYM_PITCH + lane]; };
     rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
                       act ? m_out + (base + lane) * P::K : nullptr);
     __syncwarp();
@@ -446,7 +449,11 @@ template <class P> struct PairSmem {
   static constexpr bool DSTAGE = P::level == 1;
   static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16) + (DSTAGE ? STG_UV_BYTES : 0);
   static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
-  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * 64, 16);
+#ifndef HQC_SYM_PITCH2
+#define HQC_SYM_PITCH2 68
+#endif
+  static constexpr uint32_t SYM_PITCH = HQC_SYM_PITCH2;  // 17 words (odd): conflict-free stage-2 byte stores (see WarpSmem)
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
   static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16 * 2;
   static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // index split: warp 0 takes [0, W0), warp 1 [W0, W)
 };
@@ -559,18 +566,18 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
           const uint4 x = src[c];
           X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
         }
-        sym[j * 64 + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+        sym[j * M::SYM_PITCH + s] = (uint8_t)rm_decode_block<P::MULT>(X);
       }
       PHASE(5);
       __syncthreads();
       PHASE(6);
     }
     for (uint32_t e = tid; e < P::N1 * 64; e += 64)
-      if ((e & 63) >= rows) sym[e] = 0;
+      if ((e & 63) >= rows) sym[(e >> 6) * M::SYM_PITCH + (e & 63)] = 0;
     __syncthreads();
     const uint32_t slot = 32 * wid + lane;
     const bool act = slot < rows;
-    auto sym_at = [&](int j) -> uint32_t { return sym[j * 64 + slot]; };
+    auto sym_at = [&](int j) -> uint32_t { return sym[j * M::SYM_PITCH + slot]; };
     PHASE_T0();
     if (!(HQC_EXP_SKIP & 2))
       rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(base_p + wid * S3Scratch<P>::BYTES), lane,

@@ -28,26 +28,58 @@ template <class P> constexpr int s1_unroll() {
 #endif
 }
 
-// Build E (S::E_WORDS words) from the staged dense row su (shared memory).
+// Build E (S::E_WORDS words) from the staged dense row su (shared memory):
+//   E[q] = u32[q]                                   q < Q0
+//   E[Q0] = (last C bits of u) | u32[0] << C        the wrap of X^n = 1
+//   E[q] = funnel(u32[x], u32[x + 1], 32 - C)       q = Q0 + 1 + x, x <= Q0, with u32[Q0] masked to its C
+//                                                   valid bits and u32[Q0 + 1] = 0 (bits >= n ignored, R#13)
+//   E[q] = 0                                        beyond (read only by lanes whose outputs are dropped)
+// One warp (NT = 32): su[Q0] and su[Q0 + 1] are first rewritten in place (su is a consumed staging row),
+// then each lane funnels a run of CH consecutive words (CH odd: conflict-free), loading every source
+// word once and carrying the neighbour in a register (no per-word selects). The warp pair (NT = 64)
+// keeps the strided form with per-word selects: two extra CTA barriers cost it more than the selects
+// (scripts/exp_build.py timings: HQC-1 -2% with the run form, HQC-3 +1.6%).
 template <class P, class S, int NT = 32>
-__device__ __forceinline__ void s1_build_E(const uint32_t *su, uint32_t *E, int lane) {
+__device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) {
   constexpr uint32_t NV = P::Q0 / 4;
   constexpr uint32_t MASK_C = (1u << P::C) - 1u;
-  // words below Q0: u itself
+  static_assert(P::Q0 + 1 < 2 * P::U_STRIDE, "the staged row has a padding word after word Q0");
+  const uint32_t eq0 = su[P::Q0] & MASK_C;
   for (uint32_t c = lane; c < NV; c += NT)
     reinterpret_cast<uint4 *>(E)[c] = reinterpret_cast<const uint4 *>(su)[c];
   for (uint32_t q = 4 * NV + lane; q < P::Q0; q += NT) E[q] = su[q];
-  const uint32_t eq0 = su[P::Q0] & MASK_C;  // the last C bits of u; bits >= n are ignored (R#13)
-  // word Q0: the last C bits of u, then u continues from bit 0 (the wrap of X^n = 1)
-  if (lane == 0) E[P::Q0] = eq0 | (su[0] << P::C);
-  // words above Q0: E word q holds u bits [32q - n, 32q - n + 32) = funnel(u32[x], u32[x+1], 32 - C)
-  // with x = q - Q0 - 1. Words that no valid output reads are filled with zeros.
+  if constexpr (NT == 32) {
+    constexpr uint32_t NF = P::Q0 + 1;                // funnel words x = 0..Q0
+    constexpr uint32_t CH = ((NF + NT - 1) / NT) | 1u;  // per-lane run, odd
+    const uint32_t s0 = su[0];
+    __syncwarp();  // every lane has read su[0], su[Q0] before they are rewritten
+    if (lane == 0) {
+      E[P::Q0] = eq0 | (s0 << P::C);
+      su[P::Q0] = eq0;
+      su[P::Q0 + 1] = 0u;
+    }
+    __syncwarp();
+    const uint32_t x0 = (uint32_t)lane * CH;
+    uint32_t lo = x0 < NF ? su[x0] : 0u;
 #pragma unroll 4
-  for (uint32_t q = P::Q0 + 1 + lane; q < S::E_WORDS; q += NT) {
-    const uint32_t x = q - P::Q0 - 1;
-    const uint32_t lo = x < P::Q0 ? su[x] : (x == P::Q0 ? eq0 : 0u);
-    const uint32_t hi = x + 1 < P::Q0 ? su[x + 1] : (x + 1 == P::Q0 ? eq0 : 0u);
-    E[q] = __funnelshift_r(lo, hi, 32 - P::C);
+    for (uint32_t t = 0; t < CH; t++) {
+      const uint32_t x = x0 + t;
+      if (x < NF) {
+        const uint32_t hi = su[x + 1];
+        E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+        lo = hi;
+      }
+    }
+    for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += NT) E[q] = 0u;
+  } else {
+    if (lane == 0) E[P::Q0] = eq0 | (su[0] << P::C);
+#pragma unroll 4
+    for (uint32_t q = P::Q0 + 1 + lane; q < S::E_WORDS; q += NT) {
+      const uint32_t x = q - P::Q0 - 1;
+      const uint32_t lo = x < P::Q0 ? su[x] : (x == P::Q0 ? eq0 : 0u);
+      const uint32_t hi = x + 1 < P::Q0 ? su[x + 1] : (x + 1 == P::Q0 ? eq0 : 0u);
+      E[q] = __funnelshift_r(lo, hi, 32 - P::C);
+    }
   }
 }
 
