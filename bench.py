@@ -40,6 +40,34 @@ def algorithmic_ops(p) -> dict:
                 abi_bytes=8 * p.u_stride + 8 * p.v_words + 4 * p.y_stride + p.k)
 
 
+KECCAK_OPS = 4560  # 32-bit ALU ops per Keccak-f[1600] with 3-input LOP3 and funnel shifts
+
+
+def shake_perms(msg_bytes: int, out_bytes: int) -> int:
+    """Keccak-f[1600] calls of SHAKE256 (rate 136) on msg_bytes (tag included) with out_bytes squeezed."""
+    return msg_bytes // 136 + 1 + max(0, (out_bytes + 135) // 136 - 1)
+
+
+def kem_ops(p) -> dict:
+    """Algorithmic 32-bit ALU ops per operation of the SURVEY §8(f) rows: Keccak calls
+    x KECCAK_OPS, products at 1.5 ops per (index, 32-bit word) pair, the fixed-weight sampler's
+    w(w-1)/2 compares at 2 ops each, encoders and comparisons at 1 op per word/byte."""
+    ub, vb = (p.n + 7) // 8, p.n12 // 8
+    d = p.delta
+    sampler = lambda w: 3 * w + w * (w - 1)  # noqa: E731  (map + w(w-1)/2 compares x 2)
+    enc = int(1.5 * p.wr * (p.n / 32 + p.n12 / 32)) + 2 * p.k * 2 * d + 4 * p.n1 * p.mult + 2 * p.wr
+    theta = shake_perms(32 + p.k + 1, 32) * KECCAK_OPS
+    coins = shake_perms(33, 12 * p.wr) * KECCAK_OPS + 3 * sampler(p.wr)
+    kdf = shake_perms(p.k + ub + vb + 1, 64) * KECCAK_OPS
+    cmp_ = (p.n + 31) // 32 + p.n12 // 32
+    hpk = shake_perms(2 * ub + 1, 32) * KECCAK_OPS
+    keygen = (shake_perms(33, 64) + shake_perms(33, ub) + shake_perms(33, 8 * p.w + p.k)) * KECCAK_OPS \
+        + 2 * sampler(p.w) + int(1.5 * p.w * p.n / 32) + hpk
+    dec = algorithmic_ops(p)["total"]
+    return {"encrypt": enc, "encaps": theta + coins + enc + kdf, "decaps": dec + theta + coins + enc + cmp_ + kdf,
+            "keygen": keygen, "kdf": kdf}
+
+
 def ncu_traffic(level: int, batch: int):
     """DRAM bytes (read + write) per launch of the fused kernel from the committed ncu --set full capture
     (profiles/ncu_traffic.json, scripts/ncu_traffic.py), scaled from its batch to this launch's batch."""
@@ -306,6 +334,75 @@ def side_levels(args, dev, world, rank, hdist, hqc, skip):
     return res
 
 
+def next_rows(args, dev, world, rank, hdist, hqc):
+    """SURVEY §8(f) rows 1-3 under the same protocol (device-timed, max over ranks, 65,536 rows per GPU, one
+    key per 256 ciphertexts): KeyGen from seeds, PKE Encrypt, KEM Encaps and Decaps, each with its rate and
+    its fraction of the ALU roofline (kem_ops). Decaps must accept every honest ciphertext with the
+    Encaps key."""
+    import torch
+
+    from paper_2512_12904_b200 import gen
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = 64 * sms * float(measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
+
+    def timed(fn, iters):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return hdist.max_over_ranks(e0.elapsed_time(e1), dev) / iters
+
+    def rate(n, ms, ops):
+        v = world * n / (ms / 1e3)
+        return {"value": v, "ms_per_step": ms, "batch_per_gpu": n, "alu_roofline_frac": v / world * ops / peak,
+                "ops_per_op": ops}
+
+    res = {}
+    for level in (1, 3, 5):
+        p = hqc.params(level)
+        B = 65536
+        i0, B = hdist.shard(rank, B)
+        nk = (B + 255) // 256
+        ko = kem_ops(p)
+
+        def d(a):
+            return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1)).to(dev)
+
+        def empty(nbytes):
+            return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+
+        # KeyGen is timed on B keys of its own (a batch of B/256 keys would leave most SMs idle); the
+        # first nk of them serve the KEM rows below
+        seeds = d(gen.rand_bytes(CONFIG_SEED[level], gen.TAG_TEST, i0, B, 32))
+        h, x, y, s = (empty(B * p.u_stride * 8), empty(B * p.y_stride * 4), empty(B * p.y_stride * 4),
+                      empty(B * p.u_stride * 8))
+        sigma, hpk = empty(B * p.k), empty(B * 32)
+        kg = timed(lambda: hqc.hqc_kem_keygen_batch(level, seeds, h, x, y, s, sigma, hpk), 3)
+        key = d((np.arange(B) // 256).astype(np.uint32))
+        m = d(gen.rand_bytes(CONFIG_SEED[level], gen.TAG_TEST, (1 << 24) + i0, B, p.k))
+        u, v = empty(B * p.u_stride * 8), empty(B * p.v_words * 8)
+        K1, K2, acc = empty(B * 64), empty(B * 64), empty(B)
+        ws = empty(hqc.hqc_kem_workspace_bytes(level, B))
+        enc = timed(lambda: hqc.hqc_kem_encaps_batch(level, h, s, hpk, key, m, u, v, K1, ws), 5)
+        dec = timed(lambda: hqc.hqc_kem_decaps_batch(level, h, s, hpk, sigma, key, y, u, v, K2, acc, ws), 5)
+        ok = int(acc[:B].sum().item()) == B and torch.equal(K1[: B * 64], K2[: B * 64])
+        _, r1, r2, e = gen.ct_draws(CONFIG_SEED[level], gen_shape(p), i0, B)  # valid supports (DESIGN.md §5)
+        r1, r2, e = d(r1), d(r2), d(e)
+        pke = timed(lambda: hqc.hqc_encrypt_batch(level, h, s, key, m, r1, r2, e, u, v), 5)
+        res[str(level)] = {"keygen_from_seed": rate(B, kg, ko["keygen"]), "pke_encrypt": rate(B, pke, ko["encrypt"]),
+                           "kem_encaps": rate(B, enc, ko["encaps"]), "kem_decaps": rate(B, dec, ko["decaps"]),
+                           "decaps_accepts_all_and_K_equal": bool(hdist.sum_over_ranks(
+                               torch.tensor([0 if ok else 1], device=dev)) == 0)}
+        del h, x, y, s, u, v, K1, K2, ws, r1, r2, e
+    return res
+
+
 def standalone_product(args, dev, world, rank, hdist, hqc):
     """BASELINE configs[4] second part: the standalone sparse x dense product (hqc_sparse_dense_mul_batch,
     v = NULL) at (n, w) = (17669, 66), (35851, 100), (57637, 131), against its ALU roofline (1.5 ops
@@ -466,6 +563,7 @@ def main():
     if not args.no_levels:
         out["levels"] = side_levels(args, dev, world, rank, hdist, hqc, skip=args.level)
         out["standalone_product"] = standalone_product(args, dev, world, rank, hdist, hqc)
+        out["next_rows"] = next_rows(args, dev, world, rank, hdist, hqc)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         got = hm.numpy().reshape(B, p.k)
         u = hu.numpy().view(np.uint64).reshape(B, -1)

@@ -153,10 +153,11 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
   }
 }
 
-// encrypt: one warp per ciphertext. CMP = false writes (u, v) to u_out / v_out. CMP = true is the
-// KEM's re-encryption check (kem.cuh): the re-encrypted (u', v') never leaves shared memory; it is
-// compared with the received (u_cmp, v_cmp) word by word (bits >= n of u_cmp ignored, as in
-// oracle/kem.c) with no early exit, and eq_out[ct] = 1 iff every word matched.
+// encrypt: one warp per ciphertext (the first GPU encrypt; HQC_ENC_KERNEL=1 selects it, k_encrypt2 below
+// is the default). CMP = false writes (u, v) to u_out / v_out. CMP = true is the KEM's re-encryption
+// check (kem.cuh): the re-encrypted (u', v') never leaves shared memory; it is compared with the
+// received (u_cmp, v_cmp) word by word (bits >= n of u_cmp ignored, as in oracle/kem.c) with no early
+// exit, and eq_out[2 ct] = eq_out[2 ct + 1] = 1 iff every word matched.
 template <class P, bool CMP = false>
 __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
                                                 const uint32_t *__restrict__ key_index, const uint8_t *__restrict__ m,
@@ -228,9 +229,135 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
         diff |= (x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w);
       }
       diff = __reduce_or_sync(0xffffffffu, diff);
-      if (lane == 0) eq_out[ct] = diff == 0;
+      if (lane == 0) eq_out[2 * ct] = eq_out[2 * ct + 1] = diff == 0;  // the two-flag layout of k_encrypt2
     } else {
       copy_s2g(v_out + ct * P::V_WORDS, E, P::NW, lane);
+    }
+    __syncwarp();
+  }
+}
+
+// encrypt, WARP PAIR per CTA: warp 0 computes u = r1 + h*r2, warp 1 computes v = trunc(mG + s*r2 + e),
+// concurrently and without exchanging data. Each CTA owns a contiguous range of ciphertexts, and each
+// warp keeps the doubled dense operand (E_h, E_s) of the current key in shared memory, rebuilding it only
+// when key_index changes (one key per 256 ciphertexts in the BASELINE recipe): per ciphertext only the
+// product, the encoders and the support XORs remain. CMP = true (KEM re-encryption check): each warp
+// compares its half of c' with the received c and writes its own flag, eq2_out[2 ct + warp]; the KDF
+// accepts iff both are set.
+template <class P> struct Enc2Smem {
+  using SU = FullShape<P>;
+  using SV = EncVShape<P>;
+  static constexpr uint32_t EU_BYTES = round_up(SU::E_WORDS * 4, 16);
+  static constexpr uint32_t EV_BYTES = round_up(SV::E_WORDS * 4, 16);
+  // staging of a key row (2 u_stride words), then the warp's product output
+  static constexpr uint32_t OUT_WORDS = 2 * P::U_STRIDE > P::NW ? 2 * P::U_STRIDE : P::NW;
+  static constexpr uint32_t OUT_BYTES = round_up(OUT_WORDS * 4, 16);
+  static constexpr uint32_t SUP_BYTES = round_up(P::E_STRIDE * 4, 16);
+  static constexpr uint32_t D_BYTES = round_up(round_up(P::WR, 4) * 4, 16);
+  static constexpr uint32_t MISC_BYTES = round_up(P::N1 + P::K + 16, 16);
+  static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + 2 * SUP_BYTES + D_BYTES;
+  static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + 2 * SUP_BYTES + D_BYTES + MISC_BYTES;
+  static constexpr uint32_t BYTES = W0_BYTES + W1_BYTES;
+};
+
+#ifndef HQC_ENC2_MINB
+#define HQC_ENC2_MINB 1
+#endif
+template <class P, bool CMP = false>
+__global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
+                                                 const uint32_t *__restrict__ key_index, const uint8_t *__restrict__ m,
+                                                 const uint32_t *__restrict__ r1, const uint32_t *__restrict__ r2,
+                                                 const uint32_t *__restrict__ e, uint64_t *__restrict__ u_out,
+                                                 uint64_t *__restrict__ v_out, size_t batch, size_t per,
+                                                 const uint64_t *__restrict__ u_cmp = nullptr,
+                                                 const uint64_t *__restrict__ v_cmp = nullptr,
+                                                 uint8_t *__restrict__ eq2_out = nullptr) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  using M = Enc2Smem<P>;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint8_t *base = smem + (wid ? M::W0_BYTES : 0u);
+  uint32_t *E = reinterpret_cast<uint32_t *>(base);
+  uint32_t *out = reinterpret_cast<uint32_t *>(base + (wid ? M::EV_BYTES : M::EU_BYTES));
+  uint32_t *s_r2 = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(out) + M::OUT_BYTES);
+  uint32_t *s_x = s_r2 + M::SUP_BYTES / 4;  // r1 (warp 0) or e (warp 1)
+  uint32_t *dsm = s_x + M::SUP_BYTES / 4;
+  uint8_t *cw = reinterpret_cast<uint8_t *>(dsm) + M::D_BYTES;  // warp 1 only
+  uint8_t *msg = cw + P::N1;
+  const size_t lo = (size_t)blockIdx.x * per;
+  const size_t hi = lo + per < batch ? lo + per : batch;
+  size_t cached = ~(size_t)0;
+  for (size_t ct = lo; ct < hi; ct++) {
+    const size_t key = key_index ? key_index[ct] : ct;
+    if (key != cached) {  // a public index: the only data-dependent branch, on public data
+      copy_g2s(out, (wid ? s : h) + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
+      __syncwarp();
+      if (wid) s1_build_E<P, typename M::SV>(out, E, lane);
+      else s1_build_E<P, typename M::SU>(out, E, lane);
+      cached = key;
+    }
+    copy_g2s(s_r2, r2 + ct * P::E_STRIDE, P::E_STRIDE, lane);
+    copy_g2s(s_x, (wid ? e : r1) + ct * P::E_STRIDE, P::E_STRIDE, lane);
+    if (wid)
+      for (uint32_t j = lane; j < P::K; j += 32) msg[j] = m[ct * P::K + j];
+    __syncwarp();
+    uint32_t diff = 0;
+    if (wid == 0) {  // u = r1 + h * r2 (all n bits)
+      using S = typename M::SU;
+      s1_stage_d<P, S>(s_r2, dsm, lane);
+      __syncwarp();
+      uint32_t acc[S::R];
+      s1_product<P, S>(E, dsm, acc, lane);
+      s1_store_r<S>(acc, out, lane);
+      __syncwarp();
+      xor_support_bits(out, s_x, P::WR, P::N, lane);
+      __syncwarp();
+      if (lane == 0) out[P::Q0] &= (1u << P::C) - 1u;
+      for (uint32_t q = P::Q0 + 1 + lane; q < 2 * P::U_STRIDE; q += 32) out[q] = 0;
+      __syncwarp();
+      if constexpr (CMP) {
+        const uint32_t *uc = reinterpret_cast<const uint32_t *>(u_cmp + ct * P::U_STRIDE);
+        for (uint32_t q = lane; q < 2 * P::U_WORDS; q += 32) {
+          const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & ((1u << P::C) - 1u) : 0u);
+          diff |= x ^ out[q];
+        }
+      } else {
+        copy_s2g(u_out + ct * P::U_STRIDE, out, 2 * P::U_STRIDE, lane);
+      }
+    } else {  // v = trunc(mG + s * r2 + e)
+      using S = typename M::SV;
+      rs_encode_warp<P>(msg, cw, lane);
+      s1_stage_d<P, S>(s_r2, dsm, lane);
+      __syncwarp();
+      uint32_t acc[S::R];
+      s1_product<P, S>(E, dsm, acc, lane);
+      s1_store_r<S>(acc, out, lane);
+      __syncwarp();
+      for (uint32_t j = lane; j < P::N1; j += 32) {  // RM-encode symbol j into block j, every copy
+        uint32_t w[4];
+        rm_encode_byte(cw[j], w);
+        uint32_t *blk = out + j * (P::N2 / 32);
+#pragma unroll
+        for (uint32_t c = 0; c < P::MULT; c++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) blk[4 * c + q] ^= w[q];
+      }
+      __syncwarp();
+      xor_support_bits(out, s_x, P::WR, P::N12, lane);
+      __syncwarp();
+      if constexpr (CMP) {
+        const uint4 *vc = reinterpret_cast<const uint4 *>(v_cmp + ct * P::V_WORDS);
+        for (uint32_t c = lane; c < P::NW / 4; c += 32) {
+          const uint4 x = __ldg(vc + c);
+          const uint4 y = reinterpret_cast<const uint4 *>(out)[c];
+          diff |= (x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w);
+        }
+      } else {
+        copy_s2g(v_out + ct * P::V_WORDS, out, P::NW, lane);
+      }
+    }
+    if constexpr (CMP) {
+      diff = __reduce_or_sync(0xffffffffu, diff);
+      if (lane == 0) eq2_out[2 * ct + wid] = diff == 0;
     }
     __syncwarp();
   }

@@ -7,8 +7,8 @@
 //   coins = SHAKE256(theta || 0x04, 12 wr) -> 3 wr LE u32 -> r1, r2, e        R#22 (sampler below)
 //   K     = SHAKE256((c' == c ? m' : sigma) || u bytes || v bytes || 0x03, 64) R#23
 // Decaps = the fused decrypt kernel (m') -> k_kem_coins (lane per ciphertext: theta, the coin
-// squeeze and the fixed-weight sampler) -> k_encrypt<P, true> (warp per ciphertext: re-encryption
-// compared with c inside shared memory) -> k_kem_kdf (lane per ciphertext: K). No branch on the
+// squeeze and the fixed-weight sampler) -> k_encrypt2<P, true> (warp pair per ciphertext: re-encryption
+// compared with c inside shared memory, one flag per half) -> k_kem_kdf (lane per ciphertext: K). No branch on the
 // comparison result anywhere: the KDF input is selected with masks.
 #pragma once
 #include <cstdint>
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128) k_kem_kdf(const uint8_t *__restrict__ m, 
   if (eq) {
     const size_t key = key_index ? key_index[ct] : ct;
     const uint64_t *sp = reinterpret_cast<const uint64_t *>(sigma + key * P::K);
-    const uint8_t ok = eq[ct];
+    const uint8_t ok = eq[2 * ct] & eq[2 * ct + 1];  // both halves of c' matched (k_encrypt2 flags)
     const uint64_t sel = 0ull - (uint64_t)(ok & 1u);  // all ones when accepted
 #pragma unroll
     for (uint32_t i = 0; i < KS::KW; i++) rd.f[i] = (mp[i] & sel) | (sp[i] & ~sel);
@@ -308,7 +308,7 @@ template <class P> struct KemWs {  // decaps/encaps workspace carve-up (256-byte
     r2 = r1 + r(batch * P::E_STRIDE * 4);
     e = r2 + r(batch * P::E_STRIDE * 4);
     eq = e + r(batch * P::E_STRIDE * 4);
-    total = eq + r(batch);
+    total = eq + r(2 * batch);
   }
 };
 
@@ -343,14 +343,6 @@ static int launch_kem_keygen(const uint8_t *seeds, uint64_t *h, uint32_t *x, uin
   return launch_kem_hpk<P>(h, s, hpk, nkeys, st);
 }
 
-template <class P> static int encrypt_grid(size_t batch, size_t *grid) {
-  int sms = 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
-  const size_t cap = (size_t)(sms > 0 ? sms : 148) * 16;
-  *grid = batch < cap ? batch : cap;
-  return HQC_OK;
-}
-
 template <class P>
 static int launch_kem_encaps(const uint64_t *h, const uint64_t *s, const uint8_t *hpk, const uint32_t *key,
                              const uint8_t *m, uint64_t *u, uint64_t *v, uint8_t *K_out, size_t batch, void *ws,
@@ -361,13 +353,8 @@ static int launch_kem_encaps(const uint64_t *h, const uint64_t *s, const uint8_t
            *e = reinterpret_cast<uint32_t *>(b + W.e);
   int rc = launch_kem_coins<P>(hpk, key, m, r1, r2, e, batch, st);
   if (rc) return rc;
-  const uint32_t smem = EncSmem<P>::BYTES;
-  if (cudaFuncSetAttribute(k_encrypt<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return HQC_ERR_CUDA;
-  size_t grid;
-  encrypt_grid<P>(batch, &grid);
-  k_encrypt<P, false><<<(unsigned)grid, 32, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch);
-  if (cudaGetLastError() != cudaSuccess) return HQC_ERR_CUDA;
+  rc = launch_encrypt_any<P, false>(h, s, key, m, r1, r2, e, u, v, batch, nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
   k_kem_kdf<P><<<(unsigned)((batch + 127) / 128), 128, 0, st>>>(m, nullptr, key, nullptr, u, v, K_out, nullptr, batch);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
@@ -397,13 +384,8 @@ static int launch_kem_decaps(const uint64_t *h, const uint64_t *s, const uint8_t
   if (rc) return rc;
   rc = launch_kem_coins<P>(hpk, key, mp, r1, r2, e, batch, st);
   if (rc) return rc;
-  const uint32_t smem = EncSmem<P>::BYTES;
-  if (cudaFuncSetAttribute(k_encrypt<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return HQC_ERR_CUDA;
-  size_t grid;
-  encrypt_grid<P>(batch, &grid);
-  k_encrypt<P, true><<<(unsigned)grid, 32, smem, st>>>(h, s, key, mp, r1, r2, e, nullptr, nullptr, batch, u, v, eq);
-  if (cudaGetLastError() != cudaSuccess) return HQC_ERR_CUDA;
+  rc = launch_encrypt_any<P, true>(h, s, key, mp, r1, r2, e, nullptr, nullptr, batch, u, v, eq, st);
+  if (rc) return rc;
   k_kem_kdf<P><<<(unsigned)((batch + 127) / 128), 128, 0, st>>>(mp, sigma, key, eq, u, v, K_out, acc_out, batch);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }

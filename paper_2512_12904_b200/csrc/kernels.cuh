@@ -730,22 +730,55 @@ static int launch_keygen(const uint64_t *h, const uint32_t *x, const uint32_t *y
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
+// Which encrypt kernel: 2 = warp pair with per-key cached E (k_encrypt2, default), 1 = one warp per
+// ciphertext (k_encrypt). HQC_ENC_KERNEL overrides (tests, experiments).
+static int enc_kernel() {
+  static int env = [] {
+    const char *s = getenv("HQC_ENC_KERNEL");
+    return s ? atoi(s) : 0;
+  }();
+  return env == 1 ? 1 : 2;
+}
+
+// Launch the encrypt kernel (CMP: the KEM re-encryption check writing two flags per ciphertext to eq2).
+template <class P, bool CMP>
+static int launch_encrypt_any(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m,
+                              const uint32_t *r1, const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v,
+                              size_t batch, const uint64_t *uc, const uint64_t *vc, uint8_t *eq2, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (enc_kernel() == 1) {
+    const uint32_t smem = EncSmem<P>::BYTES;
+    if (cudaFuncSetAttribute(k_encrypt<P, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return HQC_ERR_CUDA;
+    size_t grid = batch;
+    const size_t cap = (size_t)sms * 16;
+    if (grid > cap) grid = cap;
+    k_encrypt<P, CMP><<<(unsigned)grid, 32, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch, uc, vc, eq2);
+    return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+  }
+  const uint32_t smem = Enc2Smem<P>::BYTES;
+  if (cudaFuncSetAttribute(k_encrypt2<P, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return HQC_ERR_CUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encrypt2<P, CMP>, 64, smem) != cudaSuccess ||
+      per_sm < 1)
+    return HQC_ERR_CUDA;
+  const size_t cap = (size_t)sms * per_sm;
+  size_t ctas = (batch + 7) / 8;  // at least 8 ciphertexts per CTA
+  if (ctas > cap) ctas = cap;
+  const size_t per = (batch + ctas - 1) / ctas;
+  const size_t grid = (batch + per - 1) / per;
+  k_encrypt2<P, CMP><<<(unsigned)grid, 64, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch, per, uc, vc, eq2);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
 template <class P>
 static int launch_encrypt(const uint64_t *h, const uint64_t *s, const uint32_t *key, const uint8_t *m,
                           const uint32_t *r1, const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v,
                           size_t batch, cudaStream_t st) {
-  const uint32_t smem = EncSmem<P>::BYTES;
-  if (cudaFuncSetAttribute(k_encrypt<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return HQC_ERR_CUDA;
-  DevInfo *di;
-  if (cur_device(&di) < 0) return HQC_ERR_CUDA;
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  size_t grid = batch;
-  const size_t cap = (size_t)(sms > 0 ? sms : 148) * 16;
-  if (grid > cap) grid = cap;
-  k_encrypt<P><<<(unsigned)grid, 32, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch);
-  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+  return launch_encrypt_any<P, false>(h, s, key, m, r1, r2, e, u, v, batch, nullptr, nullptr, nullptr, st);
 }
 
 template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {

@@ -23,6 +23,8 @@ namespace hqc {
 template <class P> constexpr int s1_unroll() {
 #ifdef HQC_S1_UNROLL
   return HQC_S1_UNROLL;
+#elif defined(HQC_S1_UNROLL_ENC)
+  return P::level == 3 ? HQC_S1_UNROLL_ENC : (P::level == 5 ? 3 : 2);
 #else
   return P::level == 5 ? 3 : 2;
 #endif

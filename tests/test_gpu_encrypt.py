@@ -150,3 +150,52 @@ def test_scaling_config_full_size(level):
     assert torch.equal(ey.view(40, -1), Y[r0:r0 + 40]) and torch.equal(em.view(40, -1), dref.view(B, -1)[r0:r0 + 40])
     del du, dv, dy, dref, mo, U, V, Y, M
     torch.cuda.empty_cache()
+
+
+def test_one_warp_encrypt_kernel_variant():
+    """HQC_ENC_KERNEL=1 selects the first (one warp per ciphertext) encrypt kernel instead of the warp-pair
+    kernel with per-key cached operands; the encrypt and KEM parity tests run again under it in a
+    subprocess (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HQC_ENC_KERNEL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_kem.py",
+                        "tests/test_gpu_encrypt.py", "-k", "not scaling_config and not one_warp_encrypt"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_encrypt_key_switching_and_identity_rows(level):
+    """The warp-pair encrypt caches each key's doubled operands across consecutive rows of one key: rows
+    that switch keys back and forth (and runs of one key), and key_index = NULL (row b uses key b), must
+    all match the oracle's encryption."""
+    g = hqc.params(level)
+    p = oracle.params(level)
+    sh = shape_for(level)
+    nk, B = 5, 96
+    h, x, y = gen.key_draws(0x6B6579, sh, 0, nk)
+    s = np.stack([oracle.keygen(p, h[i], x[i], y[i]) for i in range(nk)])
+    H = np.zeros((nk, g.u_stride), np.uint64)
+    H[:, : h.shape[1]] = h
+    S = np.zeros_like(H)
+    S[:, : p.words] = s
+    rng = np.random.default_rng(level)
+    key = np.concatenate([rng.integers(0, nk, 40), np.repeat([3, 1, 3], [20, 5, 31])]).astype(np.uint32)
+    m, r1, r2, e = gen.ct_draws(0x6B6579, sh, 0, B)
+    ru, rv = oracle.encrypt_batch(p, h, s, key.astype(np.int64), m, r1, r2, e)
+    u = torch.empty(B * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    v = torch.empty(B * g.v_words * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_encrypt_batch(level, dev(H), dev(S), dev(key), dev(m), dev(r1), dev(r2), dev(e), u, v)
+    torch.cuda.synchronize()
+    gu, gv = host(u, np.uint64, g.u_stride), host(v, np.uint64, g.v_words)
+    assert (gu[:, : p.words] == ru).all() and (gu[:, p.words:] == 0).all()
+    assert (gv == rv).all()
+    # key_index = NULL: per-row keys
+    Hr, Sr = np.ascontiguousarray(H[key]), np.ascontiguousarray(S[key])
+    hqc.hqc_encrypt_batch(level, dev(Hr), dev(Sr), None, dev(m), dev(r1), dev(r2), dev(e), u, v)
+    torch.cuda.synchronize()
+    assert (host(u, np.uint64, g.u_stride)[:, : p.words] == ru).all() and (host(v, np.uint64, g.v_words) == rv).all()
