@@ -20,9 +20,13 @@ __constant__ uint64_t c_keccak_rc[24] = {
     0x8000000080008081ull, 0x8000000000008080ull, 0x0000000080000001ull, 0x8000000080008008ull};
 
 // Keccak-f[1600]: 24 rounds of theta, rho, pi, chi, iota on lanes A[x + 5y].
+#ifndef HQC_KECCAK_UNROLL
+#define HQC_KECCAK_UNROLL 1
+#endif
+constexpr int kKeccakUnroll = HQC_KECCAK_UNROLL;
 __device__ __forceinline__ void keccak_f1600(uint64_t (&A)[25]) {
   constexpr int RHO[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39, 41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
-#pragma unroll 1
+#pragma unroll kKeccakUnroll
   for (int round = 0; round < 24; round++) {
     uint64_t C[5], D[5], B[25];
 #pragma unroll
