@@ -452,6 +452,7 @@ def main():
     ap.add_argument("--data", default="valid", choices=["valid", "random"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=16384, help="ciphertexts per pipelined chunk of the host call")
     ap.add_argument("--no-levels", action="store_true", help="skip the per-level side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -509,7 +510,7 @@ def main():
     #      pipelines H2D, the fused kernel and D2H over two internal streams; all copies are timed
     hu, hv, hy = (t.cpu().pin_memory() for t in (du, dv, dy))
     hm = torch.empty(B * p.k, dtype=torch.uint8).pin_memory()
-    chunk = min(B, 16384)
+    chunk = min(B, args.e2e_chunk)
     ws = torch.empty(hqc.hqc_decrypt_host_workspace_bytes(args.level, chunk), dtype=torch.uint8, device=dev)
     hqc.hqc_decrypt_batch_host(args.level, hu, hv, hy, hm, ws, chunk)  # warm-up
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -522,9 +523,26 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     ems = hdist.max_over_ranks(e0.elapsed_time(e1), dev)
-    e2e = {"value": world * B * args.e2e_steps / (ems / 1e3), "unit": "decryptions/s",
-           "h2d_bytes_per_step": int(hu.numel() + hv.numel() + hy.numel()), "d2h_bytes_per_step": int(B * p.k),
-           "api": "hqc_decrypt_batch_host (pinned host buffers, chunk %d, 2 internal streams)" % chunk}
+    # the link bound of this call: pinned host -> device copy bandwidth, measured here on the same buffers
+    dbuf = torch.empty(hu.numel(), dtype=torch.uint8, device=dev)
+    dbuf.copy_(hu, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(3):
+        dbuf.copy_(hu, non_blocking=True)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * hu.numel() / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del dbuf
+    h2d_bytes = int(hu.numel() + hv.numel() + hy.numel())
+    e2e_val = world * B * args.e2e_steps / (ems / 1e3)
+    e2e = {"value": e2e_val, "unit": "decryptions/s", "h2d_bytes_per_step": h2d_bytes,
+           "d2h_bytes_per_step": int(B * p.k),
+           "api": "hqc_decrypt_batch_host (pinned host buffers, chunk %d, 2 internal streams)" % chunk,
+           "h2d_gbs_measured": h2d_gbs,
+           "link_bound_decryptions_per_s": world * h2d_gbs * 1e9 / (h2d_bytes / B),
+           "link_bound_frac": e2e_val / (world * h2d_gbs * 1e9 / (h2d_bytes / B))}
 
     ops = algorithmic_ops(p)
     peaks = measured_peaks()
