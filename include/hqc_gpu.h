@@ -204,6 +204,25 @@ int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, const uint6
                            const uint32_t *y_h, uint8_t *m_h, size_t batch, void *d_work,
                            size_t work_bytes, size_t chunk, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Serialized-ciphertext host call (the server-side end-to-end path): ct_h is a HOST array of batch
+ * ciphertexts in the serialized layout c = u bytes (ceil(n/8), LE bits) || v bytes (n1 n2 / 8), i.e.
+ * hqc_ct_bytes(p) bytes each (4,417 for HQC-1), back to back with no padding; key_h (HOST,
+ * [batch] uint32, nullable only when nkeys == 1) selects each ciphertext's key; y_keys is a DEVICE
+ * table [nkeys][y_stride] uint32 of the keys' supports (provisioned once; it stays resident); m_h is
+ * the HOST output [batch][k]. Per chunk of `chunk` ciphertexts (0 = 8192) the library copies the
+ * bytes and key indices in, unpacks them into the rows of hqc_decrypt_batch on the device
+ * (k_unpack_ct), runs the fused kernel and copies m out, pipelined over two internal streams.
+ * Key indices >= nkeys are a precondition violation (read as nkeys - 1; no fault). d_work: DEVICE
+ * workspace of at least hqc_decrypt_ct_host_workspace_bytes(p, chunk) bytes. Stream semantics as
+ * hqc_decrypt_batch_host.
+ * ------------------------------------------------------------------------------------------- */
+size_t hqc_ct_bytes(const hqc_params *p);
+size_t hqc_decrypt_ct_host_workspace_bytes(const hqc_params *p, size_t chunk);
+int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_h, const uint32_t *key_h,
+                              const uint32_t *y_keys, size_t nkeys, uint8_t *m_h, size_t batch, void *d_work,
+                              size_t work_bytes, size_t chunk, void *stream);
+
 /* Number of persistent CTAs / warps the fused kernel launches for `batch` on the current device
  * (introspection for the bench's launch accounting). Returns HQC_OK. */
 int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);

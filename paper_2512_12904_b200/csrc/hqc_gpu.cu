@@ -35,6 +35,44 @@ __global__ void k_validate_support(const uint32_t *__restrict__ y, uint32_t n, u
   }
 }
 
+// Serialized ciphertexts (c = u bytes (ceil(n/8)) || v bytes (n1 n2 / 8)) -> the ABI rows of
+// hqc_decrypt_batch: u [u_stride] and v [v_words] 64-bit words, and the ciphertext's key support row
+// from the device-resident key table. One warp per ciphertext; the byte stream has arbitrary alignment,
+// so each 32-bit word is a funnel shift of two aligned source words.
+__global__ void k_unpack_ct(const uint8_t *__restrict__ ct, size_t ct_bytes, uint32_t ub, uint32_t vb,
+                            uint32_t u_words32, uint32_t v_words32, const uint32_t *__restrict__ key,
+                            const uint32_t *__restrict__ y_keys, uint32_t nkeys, uint32_t y_stride,
+                            uint32_t *__restrict__ u_out, uint32_t *__restrict__ v_out, uint32_t *__restrict__ y_out,
+                            size_t n) {
+  const int lane = threadIdx.x & 31;
+  const size_t nw = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t stride = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t c = nw; c < n; c += stride) {
+    const size_t b0 = c * ct_bytes;
+    auto row = [&](size_t off, uint32_t nbytes, uint32_t nwords, uint32_t *dst) {
+      const size_t a = b0 + off;
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(ct + (a & ~(size_t)3));
+      const uint32_t sh = 8u * (uint32_t)(a & 3);
+      const uint32_t last = (nbytes + 3) / 4;  // source words that carry row bytes
+      for (uint32_t q = lane; q < nwords; q += 32) {
+        uint32_t w = 0;
+        if (q < last) {
+          const uint32_t lo = src[q];
+          const uint32_t hi = (4 * (q + 1) < nbytes + (sh >> 3)) ? src[q + 1] : 0u;
+          w = __funnelshift_r(lo, hi, sh);
+          if (4 * (q + 1) > nbytes) w &= 0xFFFFFFFFu >> (8 * (4 * (q + 1) - nbytes));  // bytes past the row
+        }
+        dst[q] = w;
+      }
+    };
+    row(0, ub, u_words32, u_out + c * u_words32);
+    row(ub, vb, v_words32, v_out + c * v_words32);
+    uint32_t k = key ? key[c] : 0u;
+    k = k < nkeys ? k : nkeys - 1;  // precondition key < nkeys; clamped for memory safety
+    for (uint32_t q = lane; q < y_stride; q += 32) y_out[c * y_stride + q] = y_keys[(size_t)k * y_stride + q];
+  }
+}
+
 }  // namespace hqc
 
 // ================================================================================================
@@ -345,6 +383,106 @@ extern "C" int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, 
   }
   for (int b = 0; b < 2; b++) {
     if (st[b]) cudaStreamDestroy(st[b]);  // deferred until its work completes
+    if (done[b]) cudaEventDestroy(done[b]);
+  }
+  if (start) cudaEventDestroy(start);
+  return rc;
+}
+
+// ---- serialized-ciphertext host entry point (the server-side call): host c bytes + key indices in,
+//      host m out; the keys' supports stay resident on the device
+extern "C" size_t hqc_ct_bytes(const hqc_params *p) {
+  if (check_level(p)) return 0;
+  return ((size_t)p->n + 7) / 8 + (size_t)p->n12 / 8;
+}
+
+extern "C" size_t hqc_decrypt_ct_host_workspace_bytes(const hqc_params *p, size_t chunk) {
+  if (check_level(p)) return 0;
+  auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  const size_t per = r16(hqc_ct_bytes(p) * chunk + 8) + r16(4 * chunk) + r16((size_t)p->u_stride * 8 * chunk) +
+                     r16((size_t)p->v_words * 8 * chunk) + r16((size_t)p->y_stride * 4 * chunk) +
+                     r16((size_t)p->k * chunk);
+  return 2 * per;
+}
+
+extern "C" int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_h, const uint32_t *key_h,
+                                         const uint32_t *y_keys, size_t nkeys, uint8_t *m_h, size_t batch,
+                                         void *d_work, size_t work_bytes, size_t chunk, void *stream) {
+  int s = check_level(p);
+  if (s) return s;
+  if (batch == 0) return HQC_OK;
+  if (batch > HQC_MAX_BATCH) return HQC_ERR_SIZE;
+  if (!ct_h || !y_keys || !m_h || !d_work) return HQC_ERR_NULL;
+  if (nkeys == 0 || (!key_h && nkeys != 1)) return HQC_ERR_SIZE;
+  if (misaligned(d_work) || misaligned(y_keys)) return HQC_ERR_ALIGN;
+  if (chunk == 0) chunk = 8192;
+  if (chunk > batch) chunk = batch;
+  if (work_bytes < hqc_decrypt_ct_host_workspace_bytes(p, chunk)) return HQC_ERR_SIZE;
+  auto r16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  const size_t cb = hqc_ct_bytes(p), ub = ((size_t)p->n + 7) / 8, vb = (size_t)p->n12 / 8;
+  const size_t sz[6] = {r16(cb * chunk + 8), r16(4 * chunk), r16((size_t)p->u_stride * 8 * chunk),
+                        r16((size_t)p->v_words * 8 * chunk), r16((size_t)p->y_stride * 4 * chunk),
+                        r16((size_t)p->k * chunk)};
+  uint8_t *buf[2][6];
+  uint8_t *q = static_cast<uint8_t *>(d_work);
+  for (int b = 0; b < 2; b++)
+    for (int i = 0; i < 6; i++) {
+      buf[b][i] = q;
+      q += sz[i];
+    }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t caller = (cudaStream_t)stream, st[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  int rc = HQC_OK;
+  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess)
+    rc = HQC_ERR_CUDA;
+  if (rc == HQC_OK) {
+    cudaEventRecord(start, caller);
+    cudaStreamWaitEvent(st[0], start, 0);
+    cudaStreamWaitEvent(st[1], start, 0);
+    size_t c = 0;
+    for (size_t off = 0; off < batch && rc == HQC_OK; off += chunk, c++) {
+      const size_t n = batch - off < chunk ? batch - off : chunk;
+      const int b = (int)(c & 1);
+      cudaStream_t sb = st[b];
+      if (cudaMemcpyAsync(buf[b][0], ct_h + off * cb, n * cb, cudaMemcpyHostToDevice, sb) != cudaSuccess ||
+          (key_h && cudaMemcpyAsync(buf[b][1], key_h + off, n * 4, cudaMemcpyHostToDevice, sb) != cudaSuccess)) {
+        rc = HQC_ERR_CUDA;
+        break;
+      }
+      size_t grid = (n * 32 + 255) / 256;
+      if (grid > (size_t)sms * 8) grid = (size_t)sms * 8;
+      k_unpack_ct<<<(unsigned)grid, 256, 0, sb>>>(buf[b][0], cb, (uint32_t)ub, (uint32_t)vb, 2 * p->u_stride,
+                                                  2 * p->v_words, key_h ? reinterpret_cast<const uint32_t *>(buf[b][1])
+                                                                        : nullptr,
+                                                  y_keys, (uint32_t)nkeys, p->y_stride,
+                                                  reinterpret_cast<uint32_t *>(buf[b][2]),
+                                                  reinterpret_cast<uint32_t *>(buf[b][3]),
+                                                  reinterpret_cast<uint32_t *>(buf[b][4]), n);
+      if (cudaGetLastError() != cudaSuccess) {
+        rc = HQC_ERR_CUDA;
+        break;
+      }
+      rc = hqc_decrypt_batch(p, reinterpret_cast<const uint64_t *>(buf[b][2]),
+                             reinterpret_cast<const uint64_t *>(buf[b][3]),
+                             reinterpret_cast<const uint32_t *>(buf[b][4]), buf[b][5], n, (void *)sb);
+      if (rc == HQC_OK && cudaMemcpyAsync(m_h + off * p->k, buf[b][5], n * p->k, cudaMemcpyDeviceToHost, sb) !=
+                              cudaSuccess)
+        rc = HQC_ERR_CUDA;
+    }
+    cudaEventRecord(done[0], st[0]);
+    cudaEventRecord(done[1], st[1]);
+    cudaStreamWaitEvent(caller, done[0], 0);
+    cudaStreamWaitEvent(caller, done[1], 0);
+  }
+  for (int b = 0; b < 2; b++) {
+    if (st[b]) cudaStreamDestroy(st[b]);
     if (done[b]) cudaEventDestroy(done[b]);
   }
   if (start) cudaEventDestroy(start);

@@ -87,6 +87,12 @@ def lib() -> ctypes.CDLL:
         L.hqc_decrypt_host_workspace_bytes.restype = sz
         L.hqc_decrypt_batch_host.argtypes = [P, vp, vp, vp, vp, sz, vp, sz, sz, vp]
         L.hqc_decrypt_batch_host.restype = i32
+        L.hqc_ct_bytes.argtypes = [P]
+        L.hqc_ct_bytes.restype = sz
+        L.hqc_decrypt_ct_host_workspace_bytes.argtypes = [P, sz]
+        L.hqc_decrypt_ct_host_workspace_bytes.restype = sz
+        L.hqc_decrypt_ct_batch_host.argtypes = [P, vp, vp, vp, sz, vp, sz, vp, sz, sz, vp]
+        L.hqc_decrypt_ct_batch_host.restype = i32
         L.hqc_status_str.argtypes = [i32]
         L.hqc_status_str.restype = ctypes.c_char_p
         _lib = L
@@ -296,3 +302,28 @@ def hqc_decrypt_batch_host(level: int, u, v, y_support, m_out, workspace, chunk:
     wb = workspace.numel() * workspace.element_size()
     _check(lib().hqc_decrypt_batch_host(ctypes.byref(_cp(level)), _hptr(u), _hptr(v), _hptr(y_support), _hptr(m_out),
                                         B, _ptr(workspace), wb, chunk, _stream(stream)))
+
+
+def hqc_ct_bytes(level: int) -> int:
+    """Serialized ciphertext size: ceil(n/8) + n1*n2/8 bytes."""
+    return int(lib().hqc_ct_bytes(ctypes.byref(_cp(level))))
+
+
+def hqc_decrypt_ct_host_workspace_bytes(level: int, chunk: int) -> int:
+    return int(lib().hqc_decrypt_ct_host_workspace_bytes(ctypes.byref(_cp(level)), chunk))
+
+
+def hqc_decrypt_ct_batch_host(level: int, ct, key_index, y_keys, m_out, workspace, chunk: int = 0,
+                              stream=None) -> None:
+    """The server-side end-to-end call: host serialized ciphertexts (+ host key indices, None when there
+    is one key) in, host m out; y_keys is the device-resident [nkeys][y_stride] key-support table."""
+    p = params(level)
+    B = _rows(ct, hqc_ct_bytes(level), "ct")
+    assert _rows(m_out, p.k, "m_out") == B
+    nk = _rows(y_keys, 4 * p.y_stride, "y_keys")
+    if key_index is not None:
+        assert _rows(key_index, 4, "key_index") == B
+    wb = workspace.numel() * workspace.element_size()
+    _check(lib().hqc_decrypt_ct_batch_host(ctypes.byref(_cp(level)), _hptr(ct),
+                                           None if key_index is None else _hptr(key_index), _ptr(y_keys), nk,
+                                           _hptr(m_out), B, _ptr(workspace), wb, chunk, _stream(stream)))

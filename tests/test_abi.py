@@ -54,6 +54,15 @@ def test_host_validation(L):
     L.hqc_get_params(1, ctypes.byref(p))
     a16 = ctypes.c_void_p(0x1000)
     a8 = ctypes.c_void_p(0x1008)
+    # serialized-ciphertext host call: argument checks before any CUDA work
+    assert L.hqc_ct_bytes(ctypes.byref(p)) == (p.n + 7) // 8 + p.n12 // 8 == 4417  # S:534 (HQC-1)
+    ws = L.hqc_decrypt_ct_host_workspace_bytes(ctypes.byref(p), 64)
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a16, 0, a16, 4, a16, ws, 64, None) == -4
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a16, 2, a16, 4, a16, ws, 64, None) == -4
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), None, None, a16, 1, a16, 4, a16, ws, 64, None) == -2
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a8, 1, a16, 4, a16, ws, 64, None) == -3
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a16, 1, a16, 100, a16, ws - 1, 64, None) == -4
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), None, None, None, 0, None, 0, None, 0, 0, None) == 0
     # unknown syndrome method
     assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 3, None) == -4
     assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 1, None) == 0

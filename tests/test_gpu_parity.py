@@ -314,3 +314,52 @@ def test_host_buffer_entry_point(level, chunk):
     small = torch.empty(16, dtype=torch.uint8, device=DEV)
     with pytest.raises(hqc.HqcError):
         hqc.hqc_decrypt_batch_host(level, hu, hv, hy, hm, small, chunk)
+
+
+def serialize(W, p):
+    """c = u bytes (ceil(n/8)) || v bytes (n1 n2 / 8) per row, from the ABI rows."""
+    ub = (p.n + 7) // 8
+    U = np.ascontiguousarray(W["u"]).view(np.uint8).reshape(len(W["u"]), -1)[:, :ub]
+    V = np.ascontiguousarray(W["v"]).view(np.uint8).reshape(len(W["v"]), -1)
+    return np.ascontiguousarray(np.concatenate([U, V], axis=1))
+
+
+@pytest.mark.parametrize("level,chunk", [(1, 0), (3, 37), (5, 64)])
+def test_serialized_ciphertext_host_entry_point(level, chunk):
+    """hqc_decrypt_ct_batch_host: host serialized ciphertexts (odd byte lengths, so rows start at every
+    alignment) + host key indices + the device-resident key-support table; = oracle on valid, tampered and
+    uniformly random ciphertexts, ragged last chunk; one key without key indices; the unpacked bytes past
+    n are ignored exactly like the row API's."""
+    from workloads import keys
+    p = hqc.params(level)
+    op = oracle.params(level)
+    B = 203
+    W = valid_batch(level, 60_000, B)
+    rng = np.random.default_rng(level)
+    W["v"][5] ^= np.uint64(1) << np.uint64(17)
+    W["u"][9, : op.words] = rng.integers(0, 2**63, op.words, dtype=np.uint64)
+    W["u"][9, op.words - 1] &= np.uint64((1 << (p.n % 64)) - 1)
+    W["v"][9] = rng.integers(0, 2**63, op.vwords, dtype=np.uint64)
+    ct = serialize(W, p)
+    assert ct.shape[1] == hqc.hqc_ct_bytes(level) == (p.n + 7) // 8 + p.n12 // 8
+    k0 = 60_000 // 256
+    nk = int(W["key"].max()) + 1
+    _, _, ykeys, _ = keys(level, k0, nk, {1: 0xC0F10001, 3: 0xC0F10002, 5: 0xC0F10003}[level])
+    Y = np.zeros((nk, p.y_stride), np.uint32)
+    Y[:, : p.w] = ykeys[:, : p.w]
+    hct = torch.from_numpy(ct.reshape(-1)).pin_memory()
+    hkey = torch.from_numpy(W["key"].astype(np.uint32)).pin_memory()
+    hm = torch.zeros(B * p.k, dtype=torch.uint8).pin_memory()
+    ws = torch.empty(hqc.hqc_decrypt_ct_host_workspace_bytes(level, chunk or 8192), dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_ct_batch_host(level, hct, hkey, to_dev(Y), hm, ws, chunk)
+    torch.cuda.synchronize()
+    ref = oracle.decrypt_batch(W["params"], W["u"], W["v"], W["y"])
+    got = hm.numpy().reshape(B, p.k)
+    assert (got == ref).all()
+    # one key, no key indices
+    one = W["key"] == W["key"][0]
+    ct1 = torch.from_numpy(np.ascontiguousarray(ct[one]).reshape(-1)).pin_memory()
+    hm1 = torch.zeros(int(one.sum()) * p.k, dtype=torch.uint8).pin_memory()
+    hqc.hqc_decrypt_ct_batch_host(level, ct1, None, to_dev(Y[int(W["key"][0])][None]), hm1, ws, chunk)
+    torch.cuda.synchronize()
+    assert (hm1.numpy().reshape(-1, p.k) == ref[one]).all()
