@@ -225,22 +225,26 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     lOm[i * 32 + lane] = LOGT[om];
   }
 
-  // ---- Forney on the message positions, then the output bytes
+  // ---- Forney on the message positions, then the output bytes. Omega(alpha^-j) = sum_i Omega_i alpha^{-ij}
+  //      for all k message positions at once: each log Omega_i is read once, and the exponents -ij mod 255
+  //      are compile-time constants (immediate offsets into EXPT; no modular arithmetic at run time).
+  uint32_t om_j[K];
+#pragma unroll
+  for (int j = 0; j < K; j++) om_j[j] = 0;
+#pragma unroll
+  for (int i = 0; i < TD; i++) {
+    const uint8_t *ex = EXPT + lOm[i * 32 + lane];
+#pragma unroll
+    for (int j = 0; j < K; j++) om_j[j] ^= ex[(255 - (i * j) % 255) % 255];
+  }
   uint32_t outw[K / 4];
 #pragma unroll
   for (int q = 0; q < K / 4; q++) outw[q] = 0;
 #pragma unroll
   for (int j = 0; j < K; j++) {
-    uint32_t acc = 0, e = 0;  // Omega(alpha^-j) = sum_i Omega_i alpha^{-ij}
-#pragma unroll 4
-    for (int i = 0; i < TD; i++) {
-      const uint32_t lo = lOm[i * 32 + lane];
-      acc ^= EXPT[lo + e];
-      e = mod255_sub(e, (uint32_t)j % 255u);
-    }
     const uint32_t lodd = lOdd[j * 32 + lane];
     // log e_j = log Omega(alpha^-j) - j - log Lambda_odd(alpha^-j)   (zero Omega -> e_j = 0)
-    const uint32_t lnum = LOGT[acc];
+    const uint32_t lnum = LOGT[om_j[j]];
     const uint32_t le = mod255_sub(mod255_sub(lnum == GF_LOG0 ? 0u : lnum, (uint32_t)j % 255u),
                                    lodd == GF_LOG0 ? 0u : lodd);
     const uint32_t ej = (lnum == GF_LOG0 || lodd == GF_LOG0) ? 0u : EXPT[le];
