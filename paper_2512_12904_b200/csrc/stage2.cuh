@@ -5,7 +5,8 @@
 // with bit p set) and picks the smallest a with maximal |F(a)|, sign -> bit 7. Here:
 //   1. bit-sliced copy counting: cnt_p in 2 (mult 3) or 3 (mult 5) bit planes, 32 positions per op;
 //   2. soft values -2*cnt as exact fp16 in half2 registers: register i = 16q + l holds positions
-//      (32q+l, 32q+l+16), built per bit plane with fp16 fma tricks (mostly FMA-pipe work);
+//      (32q+l, 32q+l+16); the count's bit planes are placed side by side in the mantissa and one HFMA2
+//      turns 1024 + 2^l' cnt into -2 cnt;
 //   3. the 128-point fast Walsh–Hadamard transform: 6 butterfly stages across registers (HADD2 on
 //      the FMA pipe) and one in-register stage (HFMA2 with a (1,-1) multiplier). Every value is an
 //      integer of magnitude <= 640 < 2048, so fp16 arithmetic is exact;
@@ -51,36 +52,31 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
     }
   }
 
-  // soft values v_p = -2*cnt_p (the constant mult of s_p = mult - 2 cnt_p is added to F(0) below), built
-  // per bit plane k as y_k = -2^{k+1} b_k in exact fp16 arithmetic (1 LOP3 + 1 HFMA2 per plane):
-  //   l <= 9 : x = (plane & bits{l, l+16}) | 0x6400 -> the halves are 1024 + 2^l b (mantissa bit l);
-  //            y_k = fma(x, -2^{k+1-l}, 2^{k+11-l});
-  //   10 <= l <= 14: the same on plane >> 5 (one shift per plane word) with l - 5;
-  //   l = 15 : bits 15, 31 are the fp16 sign bits: h = (plane & 0x80008000) | 1.0 = +-1 = 1 - 2b,
-  //            y_k = fma(h, 2^k, -2^k).
+  // soft values v_p = -2*cnt_p (the constant mult of s_p = mult - 2 cnt_p is added to F(0) below) as
+  // exact fp16 in one HFMA2 per register: the count's bit planes are placed side by side in the mantissa,
+  //   x = 0x6400 | plane0 bit at 2^l' | plane1 bit at 2^(l'+1) | plane2 bit at 2^(l'+2)  (per half)
+  //     = 1024 + 2^l' cnt  (<= 1024 + 128*7 < 2048: every value exact),
+  //   v = fma(x, -2^(1-l'), 2^(11-l')) = -2 cnt,
+  // with l' = l for positions l <= 7 (planes pre-shifted left by 0/1/2) and l' = l - 8 for l >= 8 (planes
+  // pre-shifted right by 8/7/6), so the three bits never leave their half. 3 LOP3 + 1 HFMA2 per register
+  // (mult 3: 2 LOP3 + 1 HFMA2).
   __half2 h[64];
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    uint32_t pls[NPL];
+    uint32_t lo[NPL], hi[NPL];
 #pragma unroll
-    for (int k = 0; k < NPL; k++) pls[k] = pl[k][q] >> 5;
+    for (int k = 0; k < NPL; k++) {
+      lo[k] = pl[k][q] << k;
+      hi[k] = pl[k][q] >> (8 - k);
+    }
 #pragma unroll
     for (int l = 0; l < 16; l++) {
-      __half2 acc;
+      const int lp = l & 7;
+      const uint32_t m0 = 0x00010001u << lp;
+      uint32_t x = and_or(l < 8 ? lo[0] : hi[0], m0, 0x64006400u);
 #pragma unroll
-      for (int k = 0; k < NPL; k++) {
-        __half2 y;
-        if (l < 15) {
-          const int lb = l <= 9 ? l : l - 5;
-          const uint32_t x = and_or(l <= 9 ? pl[k][q] : pls[k], 0x00010001u << lb, 0x64006400u);
-          y = __hfma2(u2h(x), __float2half2_rn(-ldexpf(1.0f, k + 1 - lb)), __float2half2_rn(ldexpf(1.0f, k + 11 - lb)));
-        } else {
-          const uint32_t hx = and_or(pl[k][q], 0x80008000u, 0x3C003C00u);
-          y = __hfma2(u2h(hx), __float2half2_rn(ldexpf(1.0f, k)), __float2half2_rn(-ldexpf(1.0f, k)));
-        }
-        acc = (k == 0) ? y : __hadd2(acc, y);
-      }
-      h[16 * q + l] = acc;
+      for (int k = 1; k < NPL; k++) x = and_or(l < 8 ? lo[k] : hi[k], m0 << k, x);
+      h[16 * q + l] = __hfma2(u2h(x), __float2half2_rn(-ldexpf(1.0f, 1 - lp)), __float2half2_rn(ldexpf(1.0f, 11 - lp)));
     }
   }
 
