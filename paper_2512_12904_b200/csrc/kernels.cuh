@@ -105,6 +105,7 @@ template <class P> struct S1Pipe {
     s1_build_E<P, S>(stg_u, E, lane);
     __syncwarp();
     if (v) issue_v(ct, lane);
+    else if (has_next) issue_uy(next, lane);  // no v to stage: the next rows land during this product
     uint32_t acc[S::R];
     s1_product<P, S>(E, dsm, acc, lane);
     __syncwarp();  // every lane is done reading E: r overwrites it
@@ -115,16 +116,21 @@ template <class P> struct S1Pipe {
       s1_store_r<S>(acc, E, lane);
     }
     __syncwarp();
-    if (has_next) issue_uy(next, lane);
+    if (v && has_next) issue_uy(next, lane);
   }
 };
 
 constexpr uint32_t GF_BYTES = round_up(sizeof(GfTables), 16);
 
+constexpr int WARPS_PER_CTA_S1 = 1;  // stage-1 kernel CTA size (warps)
+
 // ------------------------------------------------------------------------------------------------
 // K1: stage 1 alone. One warp per ciphertext (grid-stride over warps).
+#ifndef HQC_S1K_MINB
+#define HQC_S1K_MINB 1  // lets the compiler keep loads ahead (HQC-3 standalone product -4%)
+#endif
 template <class P>
-__global__ void __launch_bounds__(128) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
+__global__ void __launch_bounds__(32 * WARPS_PER_CTA_S1, HQC_S1K_MINB) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
                                                 const uint64_t *__restrict__ v, uint64_t *__restrict__ r_out,
                                                 size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
