@@ -48,6 +48,10 @@ __device__ __forceinline__ void keccak_f1600(uint64_t (&A)[25]) {
 
 constexpr uint32_t SHAKE256_RATE_W = 17;  // 136-byte rate = 17 lanes
 
+#ifndef HQC_SHAKE_PREFETCH  // 1: load the next absorb block during the current permutation (KEM -1.5%)
+#define HQC_SHAKE_PREFETCH 1
+#endif
+
 // Absorb a LEN-byte message into a fresh SHAKE256 state and apply the final permutation; A[0..17)
 // then holds the first 136 output bytes (call keccak_f1600 for each further block). mw(i) returns
 // message bytes [8i, 8i + 8) as a little-endian word and is called once per word, in increasing i
@@ -59,27 +63,47 @@ __device__ __forceinline__ void shake256_absorb(uint64_t (&A)[25], MsgWord &mw) 
   constexpr uint32_t LASTW = LEN / 8, NBYTE = LEN % 8;
 #pragma unroll
   for (int i = 0; i < 25; i++) A[i] = 0;
-  auto block = [&](uint32_t b) {
-#pragma unroll
-    for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) {
-      const uint32_t wi = b * SHAKE256_RATE_W + i;
-      uint64_t x = 0;
-      if (wi < LASTW) {
-        x = mw(wi);
-      } else if (wi == LASTW) {
-        if constexpr (NBYTE != 0) x = mw(wi) & ((1ull << (8 * NBYTE)) - 1ull);
-        x |= 0x1Full << (8 * NBYTE);
-      }
-      if (i == SHAKE256_RATE_W - 1 && b == NB - 1) x ^= 0x80ull << 56;
-      A[i] ^= x;
+  auto word = [&](uint32_t b, uint32_t i) -> uint64_t {  // rate word i of padded block b
+    const uint32_t wi = b * SHAKE256_RATE_W + i;
+    uint64_t x = 0;
+    if (wi < LASTW) {
+      x = mw(wi);
+    } else if (wi == LASTW) {
+      if constexpr (NBYTE != 0) x = mw(wi) & ((1ull << (8 * NBYTE)) - 1ull);
+      x |= 0x1Full << (8 * NBYTE);
     }
-    keccak_f1600(A);
+    if (i == SHAKE256_RATE_W - 1 && b == NB - 1) x ^= 0x80ull << 56;
+    return x;
   };
   if constexpr (NB == 1) {
-    block(0);
+#pragma unroll
+    for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) A[i] ^= word(0, i);
+    keccak_f1600(A);
   } else {
+#if HQC_SHAKE_PREFETCH == 1
+    // the next block's message words are loaded before the current permutation, so their (global
+    // memory) latency overlaps the 24 rounds instead of stalling the absorb
+    uint64_t nxt[SHAKE256_RATE_W];
+#pragma unroll
+    for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) nxt[i] = word(0, i);
 #pragma unroll 1
-    for (uint32_t b = 0; b < NB; b++) block(b);
+    for (uint32_t b = 0; b < NB; b++) {
+#pragma unroll
+      for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) A[i] ^= nxt[i];
+      if (b + 1 < NB) {
+#pragma unroll
+        for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) nxt[i] = word(b + 1, i);
+      }
+      keccak_f1600(A);
+    }
+#else
+#pragma unroll 1
+    for (uint32_t b = 0; b < NB; b++) {
+#pragma unroll
+      for (uint32_t i = 0; i < SHAKE256_RATE_W; i++) A[i] ^= word(b, i);
+      keccak_f1600(A);
+    }
+#endif
   }
 }
 
