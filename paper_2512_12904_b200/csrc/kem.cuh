@@ -23,8 +23,10 @@ template <class P> struct KemShape {
   static constexpr uint32_t VB = P::N12 / 8;      // serialised v bytes
   static constexpr uint32_t KW = P::K / 8;        // message words
   static constexpr uint32_t T3 = 3 * P::WR;       // coin words (u32)
-  static constexpr uint32_t PB_ROW = 33;          // u16 row pitch of the per-warp sampler buffer
-  static constexpr uint32_t PB_BYTES = round_up(T3 * PB_ROW * 2, 16);
+  // sampler buffer: per lane, 3 support segments of SEG u16 each (SEG = 4 * odd >= wr: the 32 lanes'
+  // 64-bit reads of one group index fall in 16 distinct bank pairs per half-warp); entries >= wr = 0xFFFF
+  static constexpr uint32_t SEG = ((P::WR + 3) / 4 | 1u) * 4;
+  static constexpr uint32_t PB_BYTES = round_up(32 * 3 * SEG * 2, 16);
   static_assert(P::K % 8 == 0, "messages are whole 64-bit words");
   static_assert(P::N < 65536, "sampled positions fit 16 bits");
 };
@@ -83,9 +85,9 @@ __global__ void __launch_bounds__(128) k_kem_hpk(const uint64_t *__restrict__ h,
 // ---- theta, coins and the fixed-weight sampler (lane per ciphertext; R#22):
 //   p_i = i + floor(rand_i (n - i) / 2^32), then for i = w-1 down to 0: p_i = i if p_i equals a later
 //   (already final) entry. The loop counts depend only on the level.
-// Sampled positions of the warp's 32 ciphertexts sit in shared memory as u16, row t (coin word
-// index) x column lane, row pitch 33: conflict-free both for the per-lane scan (fixed row, 32 lanes)
-// and the transposed write-out (fixed lane, 32 rows).
+// Sampled positions of the warp's 32 ciphertexts sit in shared memory as u16, per lane three contiguous
+// segments (one per support), read four at a time by the duplicate scan and row by row by the
+// transposed, coalesced write-out.
 template <class P, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS) k_kem_coins(const uint8_t *__restrict__ hpk,
                                                           const uint32_t *__restrict__ key_index,
@@ -117,6 +119,10 @@ __global__ void __launch_bounds__(32 * WARPS) k_kem_coins(const uint8_t *__restr
     rd.a = rd.b = nullptr;
     shake256_absorb<decltype(rd)::LEN>(A, rd);
   }
+  uint16_t *own = pb + lane * 3 * KS::SEG;  // this lane's three segments
+  for (uint32_t t = 0; t < 3; t++)
+#pragma unroll
+    for (uint32_t q = P::WR; q < KS::SEG; q++) own[t * KS::SEG + q] = 0xFFFFu;  // never a position (n < 65535)
   constexpr uint32_t NBLK = (KS::T3 + 2 * SHAKE256_RATE_W - 1) / (2 * SHAKE256_RATE_W);
 #pragma unroll 1
   for (uint32_t blk = 0; blk < NBLK; blk++) {
@@ -126,21 +132,38 @@ __global__ void __launch_bounds__(32 * WARPS) k_kem_coins(const uint8_t *__restr
       const uint32_t t = blk * 2 * SHAKE256_RATE_W + i;
       if (t < KS::T3) {
         const uint32_t x = (i & 1) ? (uint32_t)(A[i >> 1] >> 32) : (uint32_t)A[i >> 1];
-        const uint32_t idx = t % P::WR;
-        pb[t * KS::PB_ROW + lane] = (uint16_t)(idx + __umulhi(x, P::N - idx));
+        const uint32_t sidx = t / P::WR, idx = t % P::WR;
+        own[sidx * KS::SEG + idx] = (uint16_t)(idx + __umulhi(x, P::N - idx));
       }
     }
   }
+  // R#22 deduplication, 4 entries per 64-bit read: for i = wr-1 down to 0, p_i <- i if p_i equals a later
+  // (final) entry. Equality of four u16 at once: x = v ^ (p_i x4) has a zero halfword iff some entry
+  // matches ((x - 0x0001..) & ~x & 0x8000.. is nonzero then; a borrow can only add false positives above
+  // a true zero, so "any match" is exact). Entries <= i of the first group are forced nonzero. The loop
+  // counts depend on i only.
 #pragma unroll 1
   for (uint32_t sidx = 0; sidx < 3; sidx++) {
-    uint16_t *col = pb + sidx * P::WR * KS::PB_ROW + lane;
+    uint16_t *seg = own + sidx * KS::SEG;
+    const uint2 *seg2 = reinterpret_cast<const uint2 *>(seg);
 #pragma unroll 1
     for (int i = (int)P::WR - 1; i >= 0; i--) {
-      const uint32_t pi = col[i * KS::PB_ROW];
-      uint32_t dup = 0;
-#pragma unroll 4
-      for (uint32_t j = i + 1; j < P::WR; j++) dup |= (uint32_t)(col[j * KS::PB_ROW] == pi);
-      col[i * KS::PB_ROW] = dup ? (uint16_t)i : (uint16_t)pi;
+      const uint32_t pi = seg[i];
+      const uint32_t pp = pi * 0x00010001u;
+      const uint32_t g0 = (uint32_t)(i + 1) >> 2, nlo = (uint32_t)(i + 1) & 3u;  // entries g0*4 .. i are not later
+      const uint32_t f0 = nlo >= 1 ? 1u : 0u, f1 = nlo >= 2 ? 1u : 0u, f2 = nlo >= 3 ? 1u : 0u;
+      const uint32_t force_lo = f0 | (f1 << 16), force_hi = f2;
+      uint32_t hit = 0;
+      for (uint32_t g = g0; g < (P::WR + 3) / 4; g++) {
+        const uint2 v = seg2[g];
+        uint32_t xl = v.x ^ pp, xh = v.y ^ pp;
+        if (g == g0) {
+          xl |= force_lo;
+          xh |= force_hi;
+        }
+        hit |= ((xl - 0x00010001u) & ~xl & 0x80008000u) | ((xh - 0x00010001u) & ~xh & 0x80008000u);
+      }
+      seg[i] = hit ? (uint16_t)i : (uint16_t)pi;
     }
   }
   __syncwarp();
@@ -149,9 +172,10 @@ __global__ void __launch_bounds__(32 * WARPS) k_kem_coins(const uint8_t *__restr
 #pragma unroll 1
   for (uint32_t l = 0; l < nl; l++) {
     const size_t c = base + l;
+    const uint16_t *src = pb + l * 3 * KS::SEG;
     for (uint32_t t = lane; t < 3 * P::E_STRIDE; t += 32) {
       const uint32_t sidx = t / P::E_STRIDE, idx = t - sidx * P::E_STRIDE;
-      const uint32_t val = idx < P::WR ? pb[(sidx * P::WR + idx) * KS::PB_ROW + l] : 0u;
+      const uint32_t val = idx < P::WR ? src[sidx * KS::SEG + idx] : 0u;
       uint32_t *dst = sidx == 0 ? r1 : (sidx == 1 ? r2 : e);
       dst[c * P::E_STRIDE + idx] = val;
     }
