@@ -54,7 +54,14 @@ template <class P> struct WarpSmem {
   static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
   static constexpr uint32_t BAR_BYTES = 16;
   static constexpr uint32_t S1_BYTES = E_BYTES + STG_BYTES + D_BYTES + BAR_BYTES;  // stage-1 kernel
-  static constexpr uint32_t BYTES = S1_BYTES + SYM_BYTES;                          // fused kernel
+  // RM stage over two ciphertexts at a time when n1 leaves a mostly idle last round of 32 lanes
+  // (HQC-1: 46 blocks = 32 + 14; 92 = 3 x 32 - 4): the even ciphertext's r waits in R2
+#ifndef HQC_PAIR_S2
+#define HQC_PAIR_S2 (P::level == 1)
+#endif
+  static constexpr bool PAIR_S2 = HQC_PAIR_S2;
+  static constexpr uint32_t R2_BYTES = PAIR_S2 ? round_up(P::NW * 4, 16) : 0u;
+  static constexpr uint32_t BYTES = S1_BYTES + SYM_BYTES + R2_BYTES;               // fused kernel
 };
 
 // Per-warp stage-1 pipeline: rows of ciphertext i+1 are fetched by TMA while ciphertext i is
@@ -97,8 +104,10 @@ template <class P> struct S1Pipe {
       tma_load_1d(stg_u, v + ct * P::V_WORDS, WarpSmem<P>::VB, bar);
     }
   }
-  // Stage 1 of ciphertext ct (its u, y already requested); leaves r in E; requests next's u, y.
-  __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
+  // Stage 1 of ciphertext ct (its u, y already requested); leaves r in rout (default: E, which it may
+  // overwrite); requests next's u, y.
+  __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane, uint32_t *rout = nullptr) {
+    if (rout == nullptr) rout = E;
     wait();
     using S = DecShape<P>;
     s1_stage_d<P, S>(stg_y, dsm, lane);
@@ -111,9 +120,9 @@ template <class P> struct S1Pipe {
     __syncwarp();  // every lane is done reading E: r overwrites it
     if (v) {
       wait();  // v has landed in the staging buffer during the product loop
-      s1_store_r_xor<S>(acc, E, stg_u, lane);
+      s1_store_r_xor<S>(acc, rout, stg_u, lane);
     } else {
-      s1_store_r<S>(acc, E, lane);
+      s1_store_r<S>(acc, rout, lane);
     }
     __syncwarp();
     if (v && has_next) issue_uy(next, lane);
@@ -218,23 +227,40 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
   uint8_t *ws = smem + GF_BYTES;
   S1Pipe<P> pipe(ws, u, v, y, lane);
   uint8_t *sb = ws + WarpSmem<P>::S1_BYTES;
+  uint32_t *R2 = reinterpret_cast<uint32_t *>(sb + WarpSmem<P>::SYM_BYTES);
   const size_t lo = (size_t)blockIdx.x * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
   if (lo < hi) pipe.issue_uy(lo, lane);
+  // stage 2 of ciphertexts' RM blocks: t < N1 -> block t of (r0, slot s0); else block t - N1 of (r1, s1)
+  auto stage2 = [&](const uint32_t *r0, uint32_t s0, const uint32_t *r1, uint32_t s1, uint32_t nblk) {
+    for (uint32_t t = lane; t < nblk; t += 32) {
+      const bool second = t >= P::N1;
+      const uint32_t j = second ? t - P::N1 : t;
+      const uint4 *src = reinterpret_cast<const uint4 *>(second ? r1 : r0) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      sb[j * WarpSmem<P>::SYM_PITCH + (second ? s1 : s0)] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+  };
   for (size_t base = lo; base < hi; base += 32) {
     const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
     for (uint32_t s = 0; s < rows; s++) {
       const size_t ct = base + s;
-      pipe.run(ct, ct + 1 < hi, ct + 1, lane);
-      for (uint32_t j = lane; j < P::N1; j += 32) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
-        uint32_t X[P::MULT * 4];
-#pragma unroll
-        for (int c = 0; c < (int)P::MULT; c++) {
-          const uint4 x = src[c];
-          X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      if constexpr (WarpSmem<P>::PAIR_S2) {
+        if ((s & 1) == 0 && s + 1 < rows) {  // park r in R2; decoded together with the next one
+          pipe.run(ct, ct + 1 < hi, ct + 1, lane, R2);
+          continue;
         }
-        sb[j * WarpSmem<P>::SYM_PITCH + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+        pipe.run(ct, ct + 1 < hi, ct + 1, lane);
+        if (s & 1) stage2(R2, s - 1, pipe.E, s, 2 * P::N1);
+        else stage2(pipe.E, s, pipe.E, s, P::N1);
+      } else {
+        pipe.run(ct, ct + 1 < hi, ct + 1, lane);
+        stage2(pipe.E, s, pipe.E, s, P::N1);
       }
       __syncwarp();
     }
