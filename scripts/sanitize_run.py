@@ -57,6 +57,43 @@ def main():
         hqc.hqc_decrypt_batch_host(level, hu, hv, hy, hm, ws, 32)
         torch.cuda.synchronize()
         assert (hm.numpy().reshape(B, p.k) == ref).all(), f"host L{level}"
+        # serialized-ciphertext host call, one key
+        ub = (p.n + 7) // 8
+        one = W["key"] == W["key"][0]
+        ct = np.concatenate([W["u"][one].view(np.uint8).reshape(int(one.sum()), -1)[:, :ub],
+                             W["v"][one].view(np.uint8).reshape(int(one.sum()), -1)], axis=1)
+        hct = torch.from_numpy(np.ascontiguousarray(ct).reshape(-1)).pin_memory()
+        hm1 = torch.zeros(int(one.sum()) * p.k, dtype=torch.uint8).pin_memory()
+        wsc = torch.empty(hqc.hqc_decrypt_ct_host_workspace_bytes(level, 16), dtype=torch.uint8, device="cuda")
+        hqc.hqc_decrypt_ct_batch_host(level, hct, None, d(W["y"][np.nonzero(one)[0][:1]]), hm1, wsc, 16)
+        torch.cuda.synchronize()
+        assert (hm1.numpy().reshape(-1, p.k) == ref[one]).all(), f"ct host L{level}"
+        # step a6 in its three methods
+        for meth in ("linear", "nibble", "logexp"):
+            syn = torch.empty(B * 2 * p.delta, dtype=torch.uint8, device="cuda")
+            hqc.hqc_rs_syndromes_batch(level, s, syn, meth)
+        # KEM: keygen from seeds, H_pk, encaps, decaps
+        nk = 3
+        seeds = torch.arange(nk * 32, dtype=torch.uint8, device="cuda")
+        kh, kx, ky, ks = (torch.empty(nk * p.u_stride * 8, dtype=torch.uint8, device="cuda"),
+                          torch.empty(nk * p.y_stride * 4, dtype=torch.uint8, device="cuda"),
+                          torch.empty(nk * p.y_stride * 4, dtype=torch.uint8, device="cuda"),
+                          torch.empty(nk * p.u_stride * 8, dtype=torch.uint8, device="cuda"))
+        sig, hpk = torch.empty(nk * p.k, dtype=torch.uint8, device="cuda"), torch.empty(nk * 32, dtype=torch.uint8,
+                                                                                         device="cuda")
+        hqc.hqc_kem_keygen_batch(level, seeds, kh, kx, ky, ks, sig, hpk)
+        key = torch.from_numpy((np.arange(B) % nk).astype(np.uint32)).cuda()
+        mm = torch.from_numpy(np.ascontiguousarray(W["m"]).reshape(-1)).cuda()
+        ku, kv = torch.empty(B * p.u_stride * 8, dtype=torch.uint8, device="cuda"), torch.empty(
+            B * p.v_words * 8, dtype=torch.uint8, device="cuda")
+        K1, K2, acc = (torch.empty(B * 64, dtype=torch.uint8, device="cuda"),
+                       torch.empty(B * 64, dtype=torch.uint8, device="cuda"), torch.empty(B, dtype=torch.uint8,
+                                                                                            device="cuda"))
+        wk = torch.empty(hqc.hqc_kem_workspace_bytes(level, B), dtype=torch.uint8, device="cuda")
+        hqc.hqc_kem_encaps_batch(level, kh, ks, hpk, key, mm, ku, kv, K1, wk)
+        hqc.hqc_kem_decaps_batch(level, kh, ks, hpk, sig, key, ky, ku, kv, K2, acc, wk)
+        torch.cuda.synchronize()
+        assert int(acc.sum()) == B and torch.equal(K1, K2), f"kem L{level}"
     print("sanitize_run ok")
 
 
