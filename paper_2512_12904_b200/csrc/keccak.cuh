@@ -9,7 +9,25 @@
 
 namespace hqc {
 
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return r ? (x << r) | (x >> (64 - r)) : x; }
+// 64-bit rotation as two 32-bit funnel shifts of the register halves (r is a compile-time constant in
+// every use, so the branches fold). Written as (x << r) | (x >> (64 - r)), nvcc emitted up to four shifts
+// plus an OR for many of the rotation amounts.
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  uint32_t nl, nh;
+  if (r == 0) return x;
+  if (r < 32) {
+    nh = __funnelshift_l(lo, hi, r);
+    nl = __funnelshift_l(hi, lo, r);
+  } else if (r == 32) {
+    nh = lo;
+    nl = hi;
+  } else {
+    nh = __funnelshift_l(hi, lo, r - 32);
+    nl = __funnelshift_l(lo, hi, r - 32);
+  }
+  return ((uint64_t)nh << 32) | nl;
+}
 
 __constant__ uint64_t c_keccak_rc[24] = {
     0x0000000000000001ull, 0x0000000000008082ull, 0x800000000000808Aull, 0x8000000080008000ull,
