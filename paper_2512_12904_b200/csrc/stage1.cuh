@@ -85,12 +85,30 @@ __device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) 
   }
 }
 
+// A rotation amount d = 32 o + s is kept as (o << 7) | s: its low 5 bits are the funnel-shift amount
+// (SHF.R.W wraps the amount mod 32) and >> 5 is the window's byte offset 4 o, one shift instead of a
+// shift and a mask per index.
+// Per level from measurement: packed for the one-warp kernels (HQC-1 -1%, HQC-5 -0.5%, standalone
+// product -0.3..-0.8%), plain for the HQC-3 warp pair (+1.3% there).
+#ifndef HQC_PACK_D
+#define HQC_PACK_D (P::level != 3)
+#endif
+template <class P> __device__ __forceinline__ uint32_t s1_pack_d(uint32_t d) {
+  return HQC_PACK_D ? ((d >> 5) << 7) | (d & 31u) : d;
+}
+template <class P, class T> __device__ __forceinline__ const T *s1_window(const T *Eb, uint32_t dp) {
+  if (HQC_PACK_D)
+    return reinterpret_cast<const T *>(reinterpret_cast<const char *>(Eb) + (dp >> 5));
+  return Eb + (dp >> 5);
+}
+
 // The WT rotation amounts d_j = n - y_j from the staged support row (an entry >= n is treated as 0).
 template <class P, class S, int NT = 32>
 __device__ __forceinline__ void s1_stage_d(const uint32_t *sy, uint32_t *dsm, int lane) {
   for (uint32_t j = lane; j < S::WPAD; j += NT) {
     const uint32_t y = sy[j];
-    dsm[j] = (j < S::WT && y < P::N) ? P::N - y : P::N;
+    const uint32_t d = (j < S::WT && y < P::N) ? P::N - y : P::N;
+    dsm[j] = s1_pack_d<P>(d);
   }
 }
 
@@ -108,8 +126,8 @@ __device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32
 #pragma unroll kUnroll
   for (; j + 1 < j1; j += 2) {  // two indices per pass: one 3-input XOR per word
     const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
-    const uint32_t *p0 = Eb + (dd.x >> 5);
-    const uint32_t *p1 = Eb + (dd.y >> 5);
+    const uint32_t *p0 = s1_window<P>(Eb, dd.x);
+    const uint32_t *p1 = s1_window<P>(Eb, dd.y);
     uint32_t a0 = p0[0], b0 = p1[0];
 #pragma unroll
     for (int k = 0; k < R; k++) {
@@ -121,7 +139,7 @@ __device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32
   }
   if (j < j1) {
     const uint32_t d = dsm[j];
-    const uint32_t *p0 = Eb + (d >> 5);
+    const uint32_t *p0 = s1_window<P>(Eb, d);
     uint32_t a0 = p0[0];
 #pragma unroll
     for (int k = 0; k < R; k++) {
