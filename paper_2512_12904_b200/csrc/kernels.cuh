@@ -157,6 +157,87 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA_S1, HQC_S1K_MINB) k_stage1(
   }
 }
 
+// E built up to E_WORDS words (an E-build shape with the pair's E size)
+template <class P, uint32_t EW> struct EBuildShape {
+  static constexpr uint32_t E_WORDS = EW;
+};
+
+// K1p: stage 1 alone, WARP PAIR per CTA sharing one E, each warp computing HALF of the output words
+// over all support indices (no accumulator hand-off; R = odd ceil(n12/64)). Halving the shared memory
+// per warp doubles the resident warps of this shared-memory-bound kernel. The result goes to HBM
+// through E (both warps done reading it) with coalesced 16-byte stores.
+template <class P> struct S1PairSmem {
+  static constexpr uint32_t NWH = P::NW / 2;
+  static_assert(P::NW % 2 == 0 && (NWH % 4) == 0, "each half of r is whole 16-byte chunks");
+  using S = ProdShape<P, NWH, P::W>;
+  static constexpr uint32_t E_WORDS = round_up(P::Q0 + NWH + 32 * S::R + 2, 4);
+  static constexpr uint32_t E_BYTES = round_up(E_WORDS * 4, 16);
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
+  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + 16;
+};
+
+template <class P>
+__global__ void __launch_bounds__(64, 1) k_stage1p(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
+                                                   const uint64_t *__restrict__ v, uint64_t *__restrict__ r_out,
+                                                   size_t batch) {
+  using M = S1PairSmem<P>;
+  using S = typename M::S;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t *E = reinterpret_cast<uint32_t *>(smem);
+  uint32_t *stg_u = reinterpret_cast<uint32_t *>(smem + M::E_BYTES);
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_UV_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(smem + M::E_BYTES + M::STG_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + M::E_BYTES + M::STG_BYTES + M::D_BYTES);
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  auto issue_uy = [&](size_t ct) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, M::UB + M::YB);
+    tma_load_1d(stg_u, u + ct * P::U_STRIDE, M::UB, bar);
+    tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar);
+  };
+  size_t ct = blockIdx.x;
+  if (ct < batch && tid == 0) issue_uy(ct);
+  for (; ct < batch; ct += gridDim.x) {
+    const size_t next = ct + gridDim.x;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    s1_stage_d<P, S, 64>(stg_y, dsm, tid);
+    s1_build_E<P, EBuildShape<P, M::E_WORDS>, 64>(stg_u, E, tid);
+    __syncthreads();
+    if (tid == 0) {
+      if (v) {  // v lands in the staging buffer during the product
+        fence_proxy_async_smem();
+        mbar_expect_tx(bar, M::VB);
+        tma_load_1d(stg_u, v + ct * P::V_WORDS, M::VB, bar);
+      } else if (next < batch) {
+        issue_uy(next);
+      }
+    }
+    uint32_t acc[S::R];
+    s1_product_range<P, S>(E + wid * M::NWH, dsm, acc, lane, 0, P::W);
+    __syncthreads();  // both warps are done reading E
+    if (v) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      s1_store_r_xor<S>(acc, E + wid * M::NWH, stg_u + wid * M::NWH, lane);
+    } else {
+      s1_store_r<S>(acc, E + wid * M::NWH, lane);
+    }
+    __syncthreads();
+    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
+    const uint4 *src = reinterpret_cast<const uint4 *>(E);
+    for (uint32_t c = tid; c < P::NW / 4; c += 64) dst[c] = src[c];
+    __syncthreads();  // E and the staging buffer are free again
+    if (v && tid == 0 && next < batch) issue_uy(next);
+  }
+}
+
 // K2: stage 2 alone. One thread per RM block.
 template <class P>
 __global__ void __launch_bounds__(128) k_stage2(const uint64_t *__restrict__ r, uint8_t *__restrict__ sym,
@@ -490,10 +571,6 @@ template <class P> struct PairSmem {
   static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // index split: warp 0 takes [0, W0), warp 1 [W0, W)
 };
 
-// E built up to E_WORDS words (an E-build shape with the pair's E size)
-template <class P, uint32_t EW> struct EBuildShape {
-  static constexpr uint32_t E_WORDS = EW;
-};
 
 // Register cap per level (minimum resident CTAs): the fused kernel is latency-bound at the occupancy
 // its register count allows, so the cap trades a few registers for more resident warp pairs.
@@ -651,6 +728,17 @@ template <class P> static int dec_kernel() {
   return P::level == 3 ? 2 : 1;  // occupancy sweeps: one warp wins for HQC-1 (0.629 vs 0.645 ms) and HQC-5
 }
 template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
+// Which standalone product kernel: 1 = one warp per ciphertext (k_stage1), 2 = warp pair with the output
+// words split (k_stage1p). Measured (65,536, v = NULL): HQC-5 2.42 -> 2.14 ms with the pair; HQC-1 and
+// HQC-3 lose 0.6% / 6% (their half-width R wastes 4% / 9% of the lanes). HQC_S1_KERNEL overrides.
+template <class P> static int stage1_kernel() {
+  static int env = [] {
+    const char *s = getenv("HQC_S1_KERNEL");
+    return s ? atoi(s) : 0;
+  }();
+  if (env == 1 || env == 2) return env;
+  return P::level == 5 ? 2 : 1;
+}
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
@@ -724,6 +812,19 @@ static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  if (stage1_kernel<P>() == 2) {  // warp pair, output words split (k_stage1p)
+    const uint32_t smem = S1PairSmem<P>::BYTES;
+    if (cudaFuncSetAttribute(k_stage1p<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return HQC_ERR_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage1p<P>, 64, smem) != cudaSuccess || per_sm < 1)
+      return HQC_ERR_CUDA;
+    size_t grid = batch;
+    const size_t capp = (size_t)di->sms * per_sm;
+    if (grid > capp) grid = capp;
+    k_stage1p<P><<<(unsigned)grid, 64, smem, st>>>(u, y, v, r, batch);
+    return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+  }
   const size_t cap = (size_t)di->sms * di->cap_stage1[P::level];
   size_t grid = (batch + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
   if (grid > cap) grid = cap;

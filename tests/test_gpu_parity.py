@@ -363,3 +363,19 @@ def test_serialized_ciphertext_host_entry_point(level, chunk):
     hqc.hqc_decrypt_ct_batch_host(level, ct1, None, to_dev(Y[int(W["key"][0])][None]), hm1, ws, chunk)
     torch.cuda.synchronize()
     assert (hm1.numpy().reshape(-1, p.k) == ref[one]).all()
+
+
+@pytest.mark.parametrize("kernel", ["1", "2"])
+def test_standalone_product_kernel_variants(kernel):
+    """hqc_sparse_dense_mul_batch has two kernels (one warp per ciphertext; warp pair with the output words
+    split, the HQC-5 default); HQC_S1_KERNEL forces either (read once per process): the stage-1 parity
+    tests run again under each in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HQC_S1_KERNEL=kernel)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py",
+                        "-k", "stage1_product"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
