@@ -545,7 +545,10 @@ template <class P> struct PairSmem {
   //     1% slower than the index split on B200 (profiles/r01/NOTES.md), so it is off.
   //   else: warp w takes half of the support indices over all NW words (R = odd ceil(NW/32); exact
   //     35 for HQC-3), and warp 1 hands its accumulators to warp 0 through shared memory.
-  static constexpr bool SPLIT_WORDS = false;
+#ifndef HQC_SPLIT_WORDS
+#define HQC_SPLIT_WORDS false
+#endif
+  static constexpr bool SPLIT_WORDS = HQC_SPLIT_WORDS;
   static constexpr uint32_t NWH = P::NW / 2;
   using S = typename std::conditional<SPLIT_WORDS, ProdShape<P, P::NW / 2, P::W>, DecShape<P>>::type;
   static constexpr uint32_t EW_NEED = SPLIT_WORDS ? round_up(P::Q0 + NWH + 32 * S::R + 2, 4) : S::E_WORDS;
