@@ -10,6 +10,9 @@
  *     (3) shortened RS decoding over GF(2^8) (R#4-R#7): syndromes, Berlekamp–Massey,
  *         Chien root search over the n1 positions, Forney error values, message-first output.
  *   The results are bit-identical to the CPU oracle in oracle/ (tests/test_gpu_*.py).
+ *   Also here: step a6 alone in three GF-product methods, batched Encrypt and the KeyGen
+ *   product, KeyGen from seeds, and the HHK KEM (Encaps / Decaps with implicit rejection, SHAKE256),
+ *   plus two host-buffer end-to-end calls (ABI rows, or serialized ciphertexts with resident keys).
  *
  * Conventions for every entry point
  *   - All functions are host functions, reentrant, with no global mutable state.
