@@ -63,6 +63,10 @@ def test_host_validation(L):
     assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a8, 1, a16, 4, a16, ws, 64, None) == -3
     assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, None, a16, 1, a16, 100, a16, ws - 1, 64, None) == -4
     assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), None, None, None, 0, None, 0, None, 0, 0, None) == 0
+    # KeyGen from seeds: nkeys 0 is a no-op; NULL / misaligned arguments
+    assert L.hqc_kem_keygen_batch(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == 0
+    assert L.hqc_kem_keygen_batch(ctypes.byref(p), None, a16, a16, a16, a16, a16, None, 3, None) == -2
+    assert L.hqc_kem_keygen_batch(ctypes.byref(p), a16, a16, a16, a16, a16, a16, a8, 3, None) == -3
     # unknown syndrome method
     assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 3, None) == -4
     assert L.hqc_rs_syndromes_batch(ctypes.byref(p), None, None, 0, 1, None) == 0

@@ -379,3 +379,38 @@ def test_standalone_product_kernel_variants(kernel):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py",
                         "-k", "stage1_product"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_edge_batches_new_entry_points():
+    """batch 0 / 1 and chunk > batch on the newer entry points: step a6, KeyGen from seeds, the
+    serialized-ciphertext host call; NULL / misaligned arguments return the documented codes."""
+    level = 1
+    p = hqc.params(level)
+    op = oracle.params(level)
+    # step a6, batch 1 and 0
+    sym = np.arange(p.n1, dtype=np.uint8)[None]
+    out = torch.empty(2 * p.delta, dtype=torch.uint8, device=DEV)
+    for meth in ("linear", "nibble", "logexp"):
+        hqc.hqc_rs_syndromes_batch(level, to_dev(sym), out, meth)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy() == oracle.rs_syndromes(sym[0], p.n1, p.delta)).all()
+    hqc.hqc_rs_syndromes_batch(level, torch.empty(0, dtype=torch.uint8, device=DEV),
+                               torch.empty(0, dtype=torch.uint8, device=DEV))
+    # KeyGen from one seed
+    seeds = torch.arange(32, dtype=torch.uint8, device=DEV)
+    h, x, y, s = (torch.empty(p.u_stride * 8, dtype=torch.uint8, device=DEV), torch.empty(p.y_stride * 4, dtype=torch.uint8, device=DEV),
+                  torch.empty(p.y_stride * 4, dtype=torch.uint8, device=DEV), torch.empty(p.u_stride * 8, dtype=torch.uint8, device=DEV))
+    sig = torch.empty(16 if p.k < 16 else p.k, dtype=torch.uint8, device=DEV)[: p.k]
+    hqc.hqc_kem_keygen_batch(level, seeds, h, x, y, s, sig)  # no H_pk output
+    torch.cuda.synchronize()
+    rh, rx, ry, rs, rsig = oracle.kem_keygen(op, bytes(range(32)))
+    assert (h.cpu().numpy().view(np.uint64)[: op.words] == rh).all()
+    assert (y.cpu().numpy().view(np.uint32)[: p.w] == ry).all() and (sig.cpu().numpy() == rsig).all()
+    # serialized host call: batch 1, chunk larger than the batch
+    W = valid_batch(level, 777, 1)
+    ct = serialize(W, p)
+    hm = torch.zeros(p.k, dtype=torch.uint8).pin_memory()
+    ws = torch.empty(hqc.hqc_decrypt_ct_host_workspace_bytes(level, 1), dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_ct_batch_host(level, torch.from_numpy(ct.reshape(-1)).pin_memory(), None, to_dev(W["y"]), hm, ws, 64)
+    torch.cuda.synchronize()
+    assert (hm.numpy() == W["m"][0]).all()
