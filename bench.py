@@ -241,9 +241,21 @@ def cpu_baseline(level: int, u, v, y, got, m_ref=None, budget_s: float = 12.0) -
             mism_ref += int((m != m_ref[sl]).any(axis=1).sum())
         done += n
         n *= 2
+    # one thread too, on a short prefix of the same sample
+    n1 = min(u.shape[0], 256)
+    t0 = time.perf_counter()
+    oracle.decrypt_batch(op, u[:n1], v[:n1], y[:n1], nthreads=1)
+    one = n1 / (time.perf_counter() - t0)
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": done / t_total, "unit": "decryptions/s", "cores": cores, "kind": "oracle",
             "sample": f"first {done} ciphertexts of this rank's batch, oracle decrypt on {cores} threads "
                       f"({t_total:.1f} s)",
+            "value_1_thread": one, "cpu": model,
             "parity_mismatches_vs_gpu": mism,
             "oracle_vs_message_mismatches": mism_ref if m_ref is not None else None}
 
