@@ -30,6 +30,47 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t m, uint32_t c) {
 }
 
 
+// F = FWHT(-2 cnt) in h (register i = 16q + l holds a = 32q + l, 32q + l + 16): add the constant part,
+// take M = max |F|, and return the smallest a with |F(a)| = M (R#11) with bit 7 = [F(a) = -M].
+template <int MULT>
+__device__ __forceinline__ uint32_t rm_argmax(__half2 (&h)[64]) {
+  // a = 0: F(0) += 128 * mult (the constant part of the soft values)
+  h[0] = __hadd2(h[0], __halves2half2(__float2half(128.0f * MULT), __float2half(0.0f)));
+
+  // M = max |F| (balanced tree for ILP)
+  __half2 m[32];
+#pragma unroll
+  for (int i = 0; i < 32; i++) m[i] = __hmax2(__habs2(h[i]), __habs2(h[i + 32]));
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1)
+#pragma unroll
+    for (int i = 0; i < s; i++) m[i] = __hmax2(m[i], m[i + s]);
+  const __half Mh = __hmax(__low2half(m[0]), __high2half(m[0]));
+  const __half2 M2 = __half2half2(Mh);
+  const __half2 nM2 = __hneg2(M2);
+
+  // masks in natural order: word q = i >> 4 holds a in [32q, 32q+32); bit (i&15) + 16*half
+  uint32_t absw[4] = {0u, 0u, 0u, 0u}, posw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 64; i++) {
+    const uint32_t bit = 0x00010001u << (i & 15);
+    absw[i >> 4] |= __heq2_mask(__habs2(h[i]), M2) & bit;
+    posw[i >> 4] |= __heq2_mask(h[i], nM2) & bit;  // F(a) = -M: the codeword's bit 7 is set
+  }
+  // smallest a with |G(a)| = M (lowest set bit, lowest word first)
+  uint32_t a = 0, pw = 0;
+  bool found = false;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const bool take = !found && absw[q] != 0;
+    const uint32_t bitpos = __ffs(absw[q]) - 1;
+    a = take ? (32u * q + bitpos) : a;
+    pw = take ? (posw[q] >> bitpos) & 1u : pw;
+    found = found || take;
+  }
+  return a | (pw << 7);
+}
+
 // X[c*4 + q] = 32-bit word q of copy c of the block.
 template <int MULT>
 __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4]) {
@@ -95,41 +136,7 @@ __device__ __forceinline__ uint32_t rm_decode_block(const uint32_t (&X)[MULT * 4
   const __half2 pm = __halves2half2(__float2half(1.0f), __float2half(-1.0f));
 #pragma unroll
   for (int i = 0; i < 64; i++) h[i] = __hfma2(__high2half2(h[i]), pm, __low2half2(h[i]));
-  // a = 0: F(0) += 128 * mult (the constant part of the soft values)
-  h[0] = __hadd2(h[0], __halves2half2(__float2half(128.0f * MULT), __float2half(0.0f)));
-
-  // M = max |F| (balanced tree for ILP)
-  __half2 m[32];
-#pragma unroll
-  for (int i = 0; i < 32; i++) m[i] = __hmax2(__habs2(h[i]), __habs2(h[i + 32]));
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1)
-#pragma unroll
-    for (int i = 0; i < s; i++) m[i] = __hmax2(m[i], m[i + s]);
-  const __half Mh = __hmax(__low2half(m[0]), __high2half(m[0]));
-  const __half2 M2 = __half2half2(Mh);
-  const __half2 nM2 = __hneg2(M2);
-
-  // masks in natural order: word q = i >> 4 holds a in [32q, 32q+32); bit (i&15) + 16*half
-  uint32_t absw[4] = {0u, 0u, 0u, 0u}, posw[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-  for (int i = 0; i < 64; i++) {
-    const uint32_t bit = 0x00010001u << (i & 15);
-    absw[i >> 4] |= __heq2_mask(__habs2(h[i]), M2) & bit;
-    posw[i >> 4] |= __heq2_mask(h[i], nM2) & bit;  // F(a) = -M: the codeword's bit 7 is set
-  }
-  // smallest a with |G(a)| = M (lowest set bit, lowest word first)
-  uint32_t a = 0, pw = 0;
-  bool found = false;
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const bool take = !found && absw[q] != 0;
-    const uint32_t bitpos = __ffs(absw[q]) - 1;
-    a = take ? (32u * q + bitpos) : a;
-    pw = take ? (posw[q] >> bitpos) & 1u : pw;
-    found = found || take;
-  }
-  return a | (pw << 7);
+  return rm_argmax<MULT>(h);
 }
 
 }  // namespace hqc
