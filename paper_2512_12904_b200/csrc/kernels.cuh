@@ -784,7 +784,10 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
   const int kind = dec_kernel<P>();
   const int c = kind == 1 ? di.cap_decrypt_w1[P::level] : kind == 2 ? di.cap_decrypt[P::level] : di.cap_decrypt_ws[P::level];
   const size_t cap = (size_t)di.sms * c;
-  const size_t min_per = kind == 1 ? MIN_PER / 2 : kind == 2 ? MIN_PER : 2 * MIN_PER;
+#ifndef HQC_PAIR_MIN_PER
+#define HQC_PAIR_MIN_PER MIN_PER
+#endif
+  const size_t min_per = kind == 1 ? MIN_PER / 2 : kind == 2 ? (size_t)HQC_PAIR_MIN_PER : 2 * MIN_PER;
   size_t ctas = (batch + min_per - 1) / min_per;
   if (ctas > cap) ctas = cap;
   if (ctas == 0) ctas = 1;
