@@ -570,7 +570,14 @@ template <class P> struct PairSmem {
 #endif
   static constexpr uint32_t SYM_PITCH = HQC_SYM_PITCH2;  // 17 words (odd): conflict-free stage-2 byte stores (see WarpSmem)
   static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
-  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16 * 2;
+#ifndef HQC_PAIR_XBUF
+#define HQC_PAIR_XBUF 1
+#endif
+  // XBUF: warp 1's accumulator image in its own buffer (after the barriers) instead of above r in E,
+  // so warp 1 can store it without waiting for warp 0 to finish reading E (one CTA barrier fewer).
+  static constexpr bool XBUF = HQC_PAIR_XBUF && !SPLIT_WORDS;
+  static constexpr uint32_t XBUF_BYTES = XBUF ? round_up(P::NW * 4, 16) : 0;
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16 * 2 + XBUF_BYTES;
   static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // index split: warp 0 takes [0, W0), warp 1 [W0, W)
 };
 
@@ -650,9 +657,10 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
       } else {
         s1_product_range<P, S>(E, dsm, acc, lane, j0, j1);
         PHASE(2);
-        __syncthreads();  // both warps are done reading E
+        uint32_t *xs = M::XBUF ? reinterpret_cast<uint32_t *>(bar + 4) : E + M::XOFF;
+        if (!M::XBUF) __syncthreads();  // both warps are done reading E
         PHASE(3);
-        if (wid == 1) s1_store_r<S>(acc, E + M::XOFF, lane);
+        if (wid == 1) s1_store_r<S>(acc, xs, lane);
         __syncthreads();
         if (M::DSTAGE) {
           mbar_wait(barv, phasev);  // v of ct
@@ -661,7 +669,7 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
           mbar_wait(bar, phase);
           phase ^= 1u;
         }
-        if (wid == 0) s1_store_r_xor2<S>(acc, E, E + M::XOFF, stg_v, lane);
+        if (wid == 0) s1_store_r_xor2<S>(acc, E, xs, stg_v, lane);
       }
       __syncthreads();
       PHASE(4);
