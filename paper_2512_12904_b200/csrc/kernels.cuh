@@ -15,6 +15,7 @@
 #include "gf256.cuh"
 #include "levels.cuh"
 #include "stage1.cuh"
+#include "stage1_tmem.cuh"
 #include "stage2.cuh"
 #include "stage3.cuh"
 
@@ -740,15 +741,16 @@ template <class P> static int dec_kernel() {
 }
 template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
 // Which standalone product kernel: 1 = one warp per ciphertext (k_stage1), 2 = warp pair with the output
-// words split (k_stage1p). Measured (65,536, v = NULL): HQC-5 2.42 -> 2.14 ms with the pair; HQC-1 and
-// HQC-3 lose 0.6% / 6% (their half-width R wastes 4% / 9% of the lanes). HQC_S1_KERNEL overrides.
+// words split (k_stage1p), 3 = windows from tensor memory (k_stage1t, stage1_tmem.cuh). Measured (65,536,
+// v = NULL, ms): HQC-1 0.370 / 0.373 / 0.380, HQC-3 0.985 / 1.046 / 0.892, HQC-5 2.42 / 2.14 / 1.89.
+// HQC_S1_KERNEL overrides.
 template <class P> static int stage1_kernel() {
   static int env = [] {
     const char *s = getenv("HQC_S1_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  if (env == 1 || env == 2) return env;
-  return P::level == 5 ? 2 : 1;
+  if (env == 1 || env == 2 || env == 3) return env;
+  return P::level == 1 ? 1 : 3;  // tensor-memory windows for HQC-3/5 (-9% / -12%), one warp for HQC-1
 }
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
@@ -826,6 +828,15 @@ static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  if (stage1_kernel<P>() == 3) {  // windows from tensor memory (k_stage1t), one CTA of 8 warps per SM
+    constexpr uint32_t smem = TmS1<P>::SMEM_BYTES;
+    if (cudaFuncSetAttribute(k_stage1t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return HQC_ERR_CUDA;
+    size_t grid = (batch + TmS1<P>::WARPS - 1) / TmS1<P>::WARPS;
+    if (grid > (size_t)di->sms) grid = di->sms;
+    k_stage1t<P><<<(unsigned)grid, 32 * TmS1<P>::WARPS, smem, st>>>(u, y, v, r, batch);
+    return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+  }
   if (stage1_kernel<P>() == 2) {  // warp pair, output words split (k_stage1p)
     const uint32_t smem = S1PairSmem<P>::BYTES;
     if (cudaFuncSetAttribute(k_stage1p<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

@@ -365,7 +365,7 @@ def test_serialized_ciphertext_host_entry_point(level, chunk):
     assert (hm1.numpy().reshape(-1, p.k) == ref[one]).all()
 
 
-@pytest.mark.parametrize("kernel", ["1", "2"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3"])
 def test_standalone_product_kernel_variants(kernel):
     """hqc_sparse_dense_mul_batch has two kernels (one warp per ciphertext; warp pair with the output words
     split, the HQC-5 default); HQC_S1_KERNEL forces either (read once per process): the stage-1 parity
