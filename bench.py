@@ -445,9 +445,16 @@ def standalone_product(args, dev, world, rank, hdist, hqc):
         ops = algorithmic_ops(p)
         val = world * B / (ms / 1e3)
         nbytes = 8 * p.u_stride + 4 * p.y_stride + 8 * p.v_words
+        kern = int(os.environ.get("HQC_S1_KERNEL", "0") or 0)  # the library's choice (kernels.cuh: stage1_kernel)
+        kern = kern if kern in (1, 2, 3) else (1 if level == 1 else 3)
         res[f"n={p.n},w={p.w}"] = {"value": val, "unit": "products/s", "batch_per_gpu": B, "ms_per_step": ms,
+                                   "kernel": {1: "k_stage1 (one warp, windows from shared memory)",
+                                              2: "k_stage1p (warp pair, windows from shared memory)",
+                                              3: "k_stage1t (windows from tensor memory)"}[kern],
                                    "alu_roofline_frac": val / world * ops["stage1"] / peak,
                                    "hbm_gbs": val / world * nbytes / 1e9,
+                                   # one 4-byte shared-memory read per (index, word) pair: the bound of the
+                                   # shared-memory kernels (k_stage1t reads its windows from TMEM instead)
                                    "smem_bound_frac": val / world * ops["pairs"] / (peak / 2)}
         del du, dy, dr
     return res
@@ -611,7 +618,9 @@ def main():
            "config": {"workload": WORKLOAD[args.level], "level": args.level, "batch_per_gpu": B,
                       "global_batch": world * B, "parallelism": f"dp{world}",
                       "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB/GPU > 126 MB L2, no flush needed",
-                      "launch": {"kernel": "k_decrypt (fused, warp pair)" if gw[1] == 2 else "k_decrypt_w1 (fused, one warp)",
+                      "launch": {"kernel": {1: "k_decrypt_w1 (fused, one warp)", 2: "k_decrypt (fused, warp pair)",
+                                            4: "k_decrypt_ws (fused, warp-specialised)"}.get(
+                                                gw[1], "k_decrypt_t (fused, tensor-memory product)"),
                                  "grid": gw[0], "warps_per_cta": gw[1]}},
            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
            "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"],

@@ -358,6 +358,69 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
 }
 
 
+// K4t: fused decrypt with the product's windows in TENSOR MEMORY (stage1_tmem.cuh), one CTA per SM of
+// WARPS warps; warp g owns ciphertexts [g*per, (g+1)*per) in chunks of 32 like K4a: stage 1 (TmPipe) +
+// stage 2 per ciphertext (symbols parked as [j][slot]), then stage 3 with one lane per ciphertext.
+#ifndef HQC_DEC_T_WARPS
+#define HQC_DEC_T_WARPS (P::level == 5 ? 8 : 12)
+#endif
+template <class P> struct TmDec {
+  static constexpr int WARPS = HQC_DEC_T_WARPS;
+  static constexpr uint32_t COLS = WARPS == 16 ? 128 : (WARPS == 12 ? 160 : (WARPS == 8 ? 256 : 512));
+  static constexpr uint32_t SYM_PITCH = 36;  // odd word pitch: conflict-free stage-2 byte stores (WarpSmem)
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
+  using M = TmS1<P, WARPS, COLS, GF_BYTES + 16, SYM_BYTES, S3Scratch<P>::BYTES>;
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * TmDec<P>::WARPS, 1) k_decrypt_t(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out, size_t batch,
+                                                                        size_t per) {
+  using D = TmDec<P>;
+  using M = typename D::M;
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  gf_tables_to_smem(gf);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t ta = tm_cta_alloc<M>(smem, wib);  // (its CTA barrier also publishes the GF tables)
+  TmPipe<P, M> pipe(smem + M::PRE + (size_t)wib * M::WARP_BYTES, ta, u, v, y, lane);
+  uint8_t *sb = pipe.extra;
+  const size_t gw = (size_t)blockIdx.x * D::WARPS + wib;
+  const size_t lo = gw * per < batch ? gw * per : batch;
+  const size_t hi = lo + per < batch ? lo + per : batch;
+  if (lo < hi) pipe.fetch(lo, lane);
+  for (size_t base = lo; base < hi; base += 32) {
+    const uint32_t rows = (uint32_t)(hi - base < 32 ? hi - base : 32);
+    for (uint32_t s = 0; s < rows; s++) {
+      const size_t ct = base + s;
+      pipe.run(ct, ct + 1 < hi, ct + 1, lane);
+      for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in E)
+        const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
+        uint32_t X[P::MULT * 4];
+#pragma unroll
+        for (int c = 0; c < (int)P::MULT; c++) {
+          const uint4 x = src[c];
+          X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+        }
+        sb[j * D::SYM_PITCH + s] = (uint8_t)rm_decode_block<P::MULT>(X);
+      }
+      __syncwarp();
+    }
+    for (uint32_t s = rows; s < 32; s++)
+      for (uint32_t j = lane; j < P::N1; j += 32) sb[j * D::SYM_PITCH + s] = 0;
+    __syncwarp();
+    const bool act = (uint32_t)lane < rows;
+    auto sym_at = [&](int j) -> uint32_t { return sb[j * D::SYM_PITCH + lane]; };
+    rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
+                      act ? m_out + (base + lane) * P::K : nullptr);
+    __syncwarp();
+  }
+  tm_cta_free<M>(smem, wib);
+}
+
+
 // K4b: fused decrypt, WARP-SPECIALISED. CTA = 4 warps:
 //   warps 0-1 (product pair): per ciphertext, build E from the TMA-staged u, run the rotate-and-XOR
 //     over half of the support indices each, XOR their accumulators into a ring slot that TMA has
@@ -728,15 +791,17 @@ constexpr int DEC_THREADS = 64;   // fused kernel: one warp pair per CTA
 template <class P> static uint32_t decrypt_smem() { return GF_BYTES + PairSmem<P>::BYTES; }
 template <class P> static uint32_t decrypt_w1_smem() { return GF_BYTES + WarpSmem<P>::BYTES; }
 template <class P> static uint32_t decrypt_ws_smem() { return GF_BYTES + WsSmem<P>::BYTES; }
+template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_BYTES; }
 
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
-// 2 = warp pair, 3 = warp-specialised. HQC_DEC_KERNEL=1|2|3 overrides (experiments and tests).
+// 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t). HQC_DEC_KERNEL=1..4 overrides
+// (experiments and tests).
 template <class P> static int dec_kernel() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  if (env >= 1 && env <= 3) return env;
+  if (env >= 1 && env <= 4) return env;
   return P::level == 3 ? 2 : 1;  // occupancy sweeps: one warp wins for HQC-1 (0.629 vs 0.645 ms) and HQC-5
 }
 template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
@@ -792,6 +857,16 @@ static int cur_device(DevInfo **out) {
 constexpr size_t MIN_PER = 32;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
   const int kind = dec_kernel<P>();
+  if (kind == 4) {  // one CTA of WARPS warps per SM; at least 16 ciphertexts per warp
+    const size_t warps = (size_t)di.sms * TmDec<P>::WARPS;
+    size_t pw = (batch + warps - 1) / warps;
+    if (pw < MIN_PER / 2) pw = MIN_PER / 2;
+    *per = pw;
+    const size_t nw = (batch + pw - 1) / pw;
+    *grid = (int)((nw + TmDec<P>::WARPS - 1) / TmDec<P>::WARPS);
+    if (*grid < 1) *grid = 1;
+    return;
+  }
   const int c = kind == 1 ? di.cap_decrypt_w1[P::level] : kind == 2 ? di.cap_decrypt[P::level] : di.cap_decrypt_ws[P::level];
   const size_t cap = (size_t)di.sms * c;
 #ifndef HQC_PAIR_MIN_PER
@@ -817,6 +892,12 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
   switch (dec_kernel<P>()) {
     case 1: k_decrypt_w1<P><<<grid, 32, decrypt_w1_smem<P>(), st>>>(u, v, y, m, batch, per); break;
     case 2: k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per); break;
+    case 4:
+      if (cudaFuncSetAttribute(k_decrypt_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_t_smem<P>()) !=
+          cudaSuccess)
+        return HQC_ERR_CUDA;
+      k_decrypt_t<P><<<grid, 32 * TmDec<P>::WARPS, decrypt_t_smem<P>(), st>>>(u, v, y, m, batch, per);
+      break;
     default: k_decrypt_ws<P><<<grid, 128, decrypt_ws_smem<P>(), st>>>(u, v, y, m, batch, per); break;
   }
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
@@ -829,12 +910,12 @@ static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   if (stage1_kernel<P>() == 3) {  // windows from tensor memory (k_stage1t), one CTA of 8 warps per SM
-    constexpr uint32_t smem = TmS1<P>::SMEM_BYTES;
+    constexpr uint32_t smem = TmS1Std<P>::SMEM_BYTES;
     if (cudaFuncSetAttribute(k_stage1t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return HQC_ERR_CUDA;
-    size_t grid = (batch + TmS1<P>::WARPS - 1) / TmS1<P>::WARPS;
+    size_t grid = (batch + TmS1Std<P>::WARPS - 1) / TmS1Std<P>::WARPS;
     if (grid > (size_t)di->sms) grid = di->sms;
-    k_stage1t<P><<<(unsigned)grid, 32 * TmS1<P>::WARPS, smem, st>>>(u, y, v, r, batch);
+    k_stage1t<P><<<(unsigned)grid, 32 * TmS1Std<P>::WARPS, smem, st>>>(u, y, v, r, batch);
     return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
   }
   if (stage1_kernel<P>() == 2) {  // warp pair, output words split (k_stage1p)
@@ -945,7 +1026,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
-  *wpc = dec_kernel<P>() == 1 ? 1 : dec_kernel<P>() == 2 ? DEC_THREADS / 32 : 4;
+  *wpc = dec_kernel<P>() == 1 ? 1 : dec_kernel<P>() == 2 ? DEC_THREADS / 32 : dec_kernel<P>() == 4 ? TmDec<P>::WARPS : 4;
   return HQC_OK;
 }
 

@@ -130,132 +130,143 @@ template <class P, uint32_t V> struct TmShape {
   static constexpr uint32_t WPAD = round_up(WT, 4);
 };
 
-template <class P> struct TmS1 {
-  static constexpr uint32_t V = HQC_S1T_V;
-  using S = TmShape<P, V>;
 #ifndef HQC_S1T_WARPS
 #define HQC_S1T_WARPS (P::level == 5 ? 8 : 16)
 #endif
 #ifndef HQC_S1T_COLS
 #define HQC_S1T_COLS (P::level == 5 ? 256 : 128)
 #endif
-  static constexpr int WARPS = HQC_S1T_WARPS;         // WARPS / 4 per lane quarter
-  static constexpr uint32_t COLS = HQC_S1T_COLS;      // TMEM columns per warp
-  static constexpr uint32_t WIN = S::R + 1;           // window words per index
-#ifndef HQC_S1T_PIPE
-#define HQC_S1T_PIPE 0
-#endif
 #ifndef HQC_S1T_FU
 #define HQC_S1T_FU 2
 #endif
-  static constexpr bool PIPE = HQC_S1T_PIPE;          // prefetch the next pair's windows
+
+// Per-warp shared-memory layout of the tensor-memory product (after a per-CTA prefix of PRE bytes):
+// E | staging row (u, then v) | bucketed rotation amounts + range starts | mbarrier | EXTRA bytes (the
+// fused kernel's symbol chunk). E is at least E_MIN bytes (the fused kernel's RS scratch aliases it).
+template <class P, int WARPS_, uint32_t COLS_, uint32_t PRE_ = 16, uint32_t EXTRA_ = 0, uint32_t E_MIN_ = 0>
+struct TmS1 {
+  static constexpr uint32_t V = HQC_S1T_V;
+  using S = TmShape<P, V>;
+  static constexpr int WARPS = WARPS_;                // WARPS / 4 per lane quarter
+  static constexpr uint32_t COLS = COLS_;             // TMEM columns per warp
+  static constexpr uint32_t WIN = S::R + 1;           // window words per index
   static constexpr int FU = HQC_S1T_FU;               // refill pieces in flight
   static constexpr uint32_t G = COLS - S::R;          // word offsets per range
   static constexpr uint32_t NR = P::Q0 / G + 1;       // ranges (o = d >> 5 <= n >> 5 = Q0)
-  static constexpr uint32_t JPL = (P::W + 31) / 32;   // support slots per lane
-  // E is read by the refills up to word 31 R + (NR - 1) G + COLS - 1 (columns past a range's last
-  // window hold words no index reads; the buffer only has to be addressable there)
-  static constexpr uint32_t EW_FILL = 31 * S::R + (NR - 1) * G + COLS;
-  static constexpr uint32_t E_WORDS = round_up(EW_FILL > S::E_WORDS ? EW_FILL : S::E_WORDS, 4);
-  static constexpr uint32_t E_BYTES = E_WORDS * 4;
-  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
-  static constexpr uint32_t STG_UV_BYTES = round_up(UB > VB ? UB : VB, 16);
-#ifndef HQC_S1T_YREG
-#define HQC_S1T_YREG 1
-#endif
-  // YREG: the support row is read with plain loads into registers one ciphertext ahead (4 words per
-  // lane) instead of being staged by TMA, which frees its shared memory for more resident warps
-  static constexpr bool YREG = HQC_S1T_YREG;
-  static constexpr uint32_t STG_BYTES = STG_UV_BYTES + (YREG ? 0u : round_up(YB, 16));
+  static constexpr uint32_t JPL = (P::W + 31) / 32;   // support slots per lane (registers, one ahead)
+  // E is read by the refills up to word 31 R + (NR - 1) G + round_up(COLS, 32 FU) - 1 (columns past a
+  // range's last window hold words no index reads; the buffer only has to be addressable there)
+  static constexpr uint32_t EW_FILL = 31 * S::R + (NR - 1) * G + round_up(COLS, 32 * FU);
+  static constexpr uint32_t EW = EW_FILL > S::E_WORDS ? EW_FILL : S::E_WORDS;
+  static constexpr uint32_t E_BYTES = round_up(EW * 4 > E_MIN_ ? EW * 4 : E_MIN_, 16);
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8;
+  static constexpr uint32_t STG_BYTES = round_up(UB > VB ? UB : VB, 16);
   static constexpr uint32_t L_BYTES = round_up((S::WPAD + NR + 1) * 4, 16);  // bucketed d, then range starts
-  static constexpr uint32_t WARP_BYTES = E_BYTES + STG_BYTES + L_BYTES + 16;
+  static constexpr uint32_t EXTRA_OFF = E_BYTES + STG_BYTES + L_BYTES + 16;
+  static constexpr uint32_t WARP_BYTES = round_up(EXTRA_OFF + EXTRA_, 16);
+  static constexpr uint32_t PRE = PRE_;               // per-CTA prefix; its last 16 bytes hold the TMEM address
   // one CTA per SM: more than half of the 228 KB so that no second CTA is co-resident
-  static constexpr uint32_t SMEM_BYTES = 16 + (WARPS * WARP_BYTES > 120 * 1024 ? WARPS * WARP_BYTES : 120 * 1024);
-  static_assert(WARPS * WARP_BYTES + 16 <= 227 * 1024, "per-warp buffers fit in one CTA");
-  static_assert(COLS * (WARPS / 4) <= 512, "TMEM columns");
+  static constexpr uint32_t SMEM_BYTES = PRE + WARPS * WARP_BYTES > 120 * 1024 ? PRE + WARPS * WARP_BYTES : 120 * 1024;
+  static_assert(PRE + WARPS * WARP_BYTES <= 227 * 1024, "per-warp buffers fit in one CTA");
+  static_assert(WARPS % 4 == 0 && COLS * (WARPS / 4) <= 512 && COLS % 32 == 0, "TMEM columns");
   static_assert(G >= 32, "ranges wider than a fill piece");
   static_assert(S::R % V == 0 && G % V == 0 && (V == 1 || (V == 2 && S::R % 4 == 2) || (V == 4 && S::R % 4 == 0)),
                 "V-word aligned, conflict-free refill loads");
 };
 
-#ifndef HQC_S1T_MINB
-#define HQC_S1T_MINB 1
-#endif
-template <class P>
-__global__ void __launch_bounds__(32 * TmS1<P>::WARPS, HQC_S1T_MINB)
-    k_stage1t(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y, const uint64_t *__restrict__ v,
-              uint64_t *__restrict__ r_out, size_t batch) {
-  using M = TmS1<P>;
-  using S = typename M::S;
-  constexpr int R = S::R;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t *tm_slot = reinterpret_cast<uint32_t *>(smem);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t *ws = smem + 16 + (size_t)wib * M::WARP_BYTES;
-  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
-  uint32_t *stg_u = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
-  uint32_t *stg_y = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::STG_UV_BYTES);
-  uint32_t *list = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::STG_BYTES);
-  uint32_t *starts = list + S::WPAD;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(ws + M::E_BYTES + M::STG_BYTES + M::L_BYTES);
+// CTA start: warp 0 allocates all 512 TMEM columns (one CTA per SM), every lane learns its warp's base.
+template <class M> __device__ __forceinline__ uint32_t tm_cta_alloc(uint8_t *smem, int wib) {
+  uint32_t *slot = reinterpret_cast<uint32_t *>(smem + M::PRE - 16);
   if (wib == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tm_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (lane == 0) mbar_init(bar, 1);
   tm_fence_before();
   __syncthreads();
   tm_fence_after();
   // this warp's TMEM: lanes 32 (w % 4) .. + 31, columns (w / 4) * COLS .. + COLS - 1
-  const uint32_t ta = *tm_slot + ((uint32_t)(32 * (wib & 3)) << 16) + (uint32_t)(wib >> 2) * M::COLS;
-  uint32_t phase = 0;
-  auto issue_uy = [&](size_t ct) {
+  return *slot + ((uint32_t)(32 * (wib & 3)) << 16) + (uint32_t)(wib >> 2) * M::COLS;
+}
+template <class M> __device__ __forceinline__ void tm_cta_free(uint8_t *smem, int wib) {
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  if (wib == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(
+        *reinterpret_cast<uint32_t *>(smem + M::PRE - 16)));
+}
+
+// One warp's product pipeline: u of the current ciphertext staged by TMA, its support in registers
+// (loaded one ciphertext ahead), the windows from this warp's TMEM columns.
+template <class P, class M> struct TmPipe {
+  using S = typename M::S;
+  static constexpr int R = S::R;
+  uint32_t *E, *stg, *list, *starts;
+  uint64_t *bar;
+  uint8_t *extra;
+  uint32_t phase, ta;
+  uint32_t yn[M::JPL];
+  const uint64_t *u, *v;
+  const uint32_t *y;
+
+  __device__ __forceinline__ TmPipe(uint8_t *ws, uint32_t ta_, const uint64_t *u_, const uint64_t *v_,
+                                    const uint32_t *y_, int lane)
+      : ta(ta_), u(u_), v(v_), y(y_) {
+    E = reinterpret_cast<uint32_t *>(ws);
+    stg = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
+    list = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::STG_BYTES);
+    starts = list + S::WPAD;
+    bar = reinterpret_cast<uint64_t *>(ws + M::E_BYTES + M::STG_BYTES + M::L_BYTES);
+    extra = ws + M::EXTRA_OFF;
+    phase = 0;
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+  }
+  __device__ __forceinline__ void wait() {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+  }
+  __device__ __forceinline__ void tma_row(const void *src, uint32_t bytes, int lane) {
     if (lane == 0) {
       fence_proxy_async_smem();
-      mbar_expect_tx(bar, M::UB + (M::YREG ? 0u : M::YB));
-      tma_load_1d(stg_u, u + ct * P::U_STRIDE, M::UB, bar);
-      if (!M::YREG) tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar);
+      mbar_expect_tx(bar, bytes);
+      tma_load_1d(stg, src, bytes, bar);
     }
-  };
-  const size_t nwarps = (size_t)gridDim.x * M::WARPS;
-  size_t ct = (size_t)blockIdx.x * M::WARPS + wib;
-  uint32_t yn[M::JPL];
-  auto load_y = [&](size_t c) {
+  }
+  // request ciphertext ct's u (TMA) and its support row (registers)
+  __device__ __forceinline__ void fetch(size_t ct, int lane) {
+    tma_row(u + ct * P::U_STRIDE, M::UB, lane);
 #pragma unroll
     for (uint32_t s = 0; s < M::JPL; s++) {
       const uint32_t j = lane + 32 * s;
-      yn[s] = j < P::W ? __ldg(y + c * P::Y_STRIDE + j) : 0u;
+      yn[s] = j < P::W ? __ldg(y + ct * P::Y_STRIDE + j) : 0u;
     }
-  };
-  if (ct < batch) {
-    issue_uy(ct);
-    if (M::YREG) load_y(ct);
   }
-  for (; ct < batch; ct += nwarps) {
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    // rotation amounts d_j = n - y_j (an entry >= n counts as y = 0, R#13), bucketed by range
+
+  // Stage 1 of ciphertext ct (fetched): leaves r = v XOR trunc(u * y) (or the product alone when v is
+  // NULL) in E[0 .. NW); requests `next` when has_next (v: after r is stored, else during the product).
+  __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
+    wait();
+    // rotation amounts d_j = n - y_j (an entry >= n counts as y = 0, R#13) and their ranges
     uint32_t dj[M::JPL], tj[M::JPL];
 #pragma unroll
     for (uint32_t s = 0; s < M::JPL; s++) {
       const uint32_t j = lane + 32 * s;
-      const uint32_t yy = M::YREG ? yn[s] : (j < P::W ? stg_y[j] : 0u);
-      dj[s] = yy < P::N ? P::N - yy : P::N;
+      dj[s] = yn[s] < P::N ? P::N - yn[s] : P::N;
       tj[s] = j < P::W ? (dj[s] >> 5) / M::G : M::NR;
     }
-    if (M::YREG && ct + nwarps < batch) load_y(ct + nwarps);  // in flight during this product
-    s1_build_E<P, S>(stg_u, E, lane);
+    s1_build_E<P, S>(stg, E, lane);
     __syncwarp();
-    if (v) {  // v lands in the (consumed) staging row during the product
-      if (lane == 0) {
-        fence_proxy_async_smem();
-        mbar_expect_tx(bar, M::VB);
-        tma_load_1d(stg_u, v + ct * P::V_WORDS, M::VB, bar);
+    if (v) tma_row(v + ct * P::V_WORDS, M::VB, lane);  // v lands in the consumed staging row
+    else if (has_next) tma_row(u + next * P::U_STRIDE, M::UB, lane);
+    if (has_next) {
+#pragma unroll
+      for (uint32_t s = 0; s < M::JPL; s++) {  // in flight during this product
+        const uint32_t j = lane + 32 * s;
+        yn[s] = j < P::W ? __ldg(y + next * P::Y_STRIDE + j) : 0u;
       }
-    } else if (ct + nwarps < batch) {
-      issue_uy(ct + nwarps);
     }
-    {
+    {  // bucket by range: ballot compaction, range by range (w entries in total, whatever the split)
       uint32_t pos = 0;
       const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 1
@@ -277,12 +288,12 @@ __global__ void __launch_bounds__(32 * TmS1<P>::WARPS, HQC_S1T_MINB)
     const uint32_t *Erow = E + lane * R;
 #pragma unroll 1
     for (uint32_t t = 0; t < M::NR; t++) {
-      // refill: row l, column c <- E[l R + t G + c]; FU pieces of 32 words loaded before their stores
-      const uint32_t *src = Erow + t * M::G;  // V-word aligned: R, G and c are multiples of V
-#pragma unroll 1
-      // columns this range's windows reach: (min(t G + G - 1, Q0) - t G) + WIN (the last range is short)
+      // refill: row l, column c <- E[l R + t G + c], the columns this range's windows reach:
+      // (min(t G + G - 1, Q0) - t G) + WIN (the last range is short); FU pieces of 32 in flight
       const uint32_t omax = (t + 1) * M::G - 1 < P::Q0 ? (t + 1) * M::G - 1 : P::Q0;
       const uint32_t nc = omax - t * M::G + M::WIN;
+      const uint32_t *src = Erow + t * M::G;  // V-word aligned: R, G and c are multiples of V
+#pragma unroll 1
       for (uint32_t c = 0; c < nc; c += 32 * M::FU) {
         uint32_t f[M::FU][32];
 #pragma unroll
@@ -306,45 +317,15 @@ __global__ void __launch_bounds__(32 * TmS1<P>::WARPS, HQC_S1T_MINB)
       tm_wait_st();
       const uint32_t j1 = starts[t + 1], tg = t * M::G;
       uint32_t j = starts[t];
-      auto pair = [&](const uint32_t (&a)[2][M::WIN], uint32_t d0, uint32_t d1) {
+#pragma unroll 1
+      for (; j + 1 < j1; j += 2) {  // two indices per pass: one 3-input XOR per word
+        const uint32_t d0 = list[j], d1 = list[j + 1];
+        uint32_t a[M::WIN], b[M::WIN];
+        tm_ld_n<M::WIN>(a, ta + (d0 >> 5) - tg);
+        tm_ld_n<M::WIN>(b, ta + (d1 >> 5) - tg);
+        tm_wait_ld();
 #pragma unroll
-        for (int k = 0; k < R; k++)
-          acc[k] ^= __funnelshift_r(a[0][k], a[0][k + 1], d0) ^ __funnelshift_r(a[1][k], a[1][k + 1], d1);
-      };
-      auto load = [&](uint32_t (&a)[2][M::WIN], uint32_t d0, uint32_t d1) {
-        tm_ld_n<M::WIN>(a[0], ta + (d0 >> 5) - tg);
-        tm_ld_n<M::WIN>(a[1], ta + (d1 >> 5) - tg);
-      };
-      if constexpr (M::PIPE) {
-        // two pair buffers: the next pair's windows are in flight while this pair is combined
-        uint32_t A[2][M::WIN], B[2][M::WIN];
-        if (j + 1 < j1) load(A, list[j], list[j + 1]);
-#pragma unroll 1
-        while (j + 1 < j1) {
-          tm_wait_ld();
-          const uint32_t a0 = list[j], a1 = list[j + 1];
-          const bool nb = j + 3 < j1;
-          if (nb) load(B, list[j + 2], list[j + 3]);
-          pair(A, a0, a1);
-          j += 2;
-          if (!nb) break;
-          tm_wait_ld();
-          const uint32_t b0 = list[j], b1 = list[j + 1];
-          const bool na = j + 3 < j1;
-          if (na) load(A, list[j + 2], list[j + 3]);
-          pair(B, b0, b1);
-          j += 2;
-          if (!na) break;
-        }
-      } else {
-#pragma unroll 1
-        for (; j + 1 < j1; j += 2) {
-          const uint32_t d0 = list[j], d1 = list[j + 1];
-          uint32_t a[2][M::WIN];
-          load(a, d0, d1);
-          tm_wait_ld();
-          pair(a, d0, d1);
-        }
+        for (int k = 0; k < R; k++) acc[k] ^= __funnelshift_r(a[k], a[k + 1], d0) ^ __funnelshift_r(b[k], b[k + 1], d1);
       }
       if (j < j1) {
         const uint32_t d0 = list[j];
@@ -357,23 +338,42 @@ __global__ void __launch_bounds__(32 * TmS1<P>::WARPS, HQC_S1T_MINB)
     }
     __syncwarp();  // every lane's refills have read E: r overwrites it
     if (v) {
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      s1_store_r_xor<S>(acc, E, stg_u, lane);
+      wait();
+      s1_store_r_xor<S>(acc, E, stg, lane);
     } else {
       s1_store_r<S>(acc, E, lane);
     }
     __syncwarp();
-    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
-    const uint4 *srcv = reinterpret_cast<const uint4 *>(E);
-    for (uint32_t c = lane; c < P::NW / 4; c += 32) dst[c] = srcv[c];
-    __syncwarp();
-    if (v && ct + nwarps < batch) issue_uy(ct + nwarps);
+    if (v && has_next) tma_row(u + next * P::U_STRIDE, M::UB, lane);  // staging row free again
   }
-  tm_fence_before();
-  __syncthreads();
-  tm_fence_after();
-  if (wib == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tm_slot));
+};
+
+template <class P> using TmS1Std = TmS1<P, HQC_S1T_WARPS, HQC_S1T_COLS>;
+
+#ifndef HQC_S1T_MINB
+#define HQC_S1T_MINB 1
+#endif
+// K1t: stage 1 alone, one warp per ciphertext (grid-stride over the CTA's warps), one CTA per SM.
+template <class P>
+__global__ void __launch_bounds__(32 * TmS1Std<P>::WARPS, HQC_S1T_MINB)
+    k_stage1t(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y, const uint64_t *__restrict__ v,
+              uint64_t *__restrict__ r_out, size_t batch) {
+  using M = TmS1Std<P>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t ta = tm_cta_alloc<M>(smem, wib);
+  TmPipe<P, M> pipe(smem + M::PRE + (size_t)wib * M::WARP_BYTES, ta, u, v, y, lane);
+  const size_t nwarps = (size_t)gridDim.x * M::WARPS;
+  size_t ct = (size_t)blockIdx.x * M::WARPS + wib;
+  if (ct < batch) pipe.fetch(ct, lane);
+  for (; ct < batch; ct += nwarps) {
+    pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
+    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
+    const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E);
+    for (uint32_t c = lane; c < P::NW / 4; c += 32) dst[c] = src[c];
+    __syncwarp();
+  }
+  tm_cta_free<M>(smem, wib);
 }
 
 }  // namespace hqc

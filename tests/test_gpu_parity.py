@@ -267,10 +267,11 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
-    """The library picks the warp-pair kernel (HQC-1/3) or the one-warp kernel (HQC-5) per level;
-    HQC_DEC_KERNEL forces either (read once per process), so each runs in a subprocess on every level."""
+    """The library picks the warp-pair kernel (HQC-3) or the one-warp kernel (HQC-1/5) per level; the
+    warp-specialised kernel (3) and the tensor-memory-product kernel (4) are alternatives. HQC_DEC_KERNEL
+    forces each (read once per process), so each runs in a subprocess on every level."""
     import subprocess
     import sys
     import os
