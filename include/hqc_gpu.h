@@ -93,8 +93,9 @@ int hqc_decrypt_batch(const hqc_params *p, const uint64_t *u, const uint64_t *v,
 /* Stage 1 alone (Eq. 1; truncation R#3):
  *   r_out[b] = v[b] XOR trunc_{n12}(u[b] * y[b]), [batch][v_words] uint64.
  *   v may be NULL: r_out is then the truncated product alone (the standalone sparse x dense
- *   product of BASELINE configs[4]). HQC-3/5 read the product's windows from tensor memory
- *   (tcgen05.ld; one CTA per SM holding the TMEM allocation), HQC-1 from shared memory. */
+ *   product of BASELINE configs[4]). Constant-flow (fixed loop counts, R#8); the environment
+ *   variable HQC_S1_KERNEL=3 selects a faster tensor-memory kernel whose loop counts depend on
+ *   y. */
 int hqc_sparse_dense_mul_batch(const hqc_params *p, const uint64_t *u, const uint32_t *y_support,
                                const uint64_t *v, uint64_t *r_out, size_t batch, void *stream);
 

@@ -808,14 +808,15 @@ template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
 // Which standalone product kernel: 1 = one warp per ciphertext (k_stage1), 2 = warp pair with the output
 // words split (k_stage1p), 3 = windows from tensor memory (k_stage1t, stage1_tmem.cuh). Measured (65,536,
 // v = NULL, ms): HQC-1 0.370 / 0.373 / 0.380, HQC-3 0.985 / 1.046 / 0.892, HQC-5 2.42 / 2.14 / 1.89.
-// HQC_S1_KERNEL overrides.
+// The default stays constant-flow (R#8): k_stage1t buckets the support by offset range, so its
+// per-range trip counts depend on y; it is opt-in (HQC_S1_KERNEL=3) for inputs whose timing may leak.
 template <class P> static int stage1_kernel() {
   static int env = [] {
     const char *s = getenv("HQC_S1_KERNEL");
     return s ? atoi(s) : 0;
   }();
   if (env == 1 || env == 2 || env == 3) return env;
-  return P::level == 1 ? 1 : 3;  // tensor-memory windows for HQC-3/5 (-9% / -12%), one warp for HQC-1
+  return P::level == 5 ? 2 : 1;
 }
 template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {

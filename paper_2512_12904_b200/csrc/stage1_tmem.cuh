@@ -1,7 +1,13 @@
 // Stage 1 (the sparse x dense product of Eq. 1, §III.B) with its windows read from TENSOR
-// MEMORY instead of shared memory: K1t, the standalone product behind hqc_sparse_dense_mul_batch
-// (HQC_S1_KERNEL=3). Same arithmetic as stage1.cuh (r[W] ^= SHF(E[o + W], E[o + W + 1], s) for each
-// support index, o = d >> 5, s = d & 31), different load path.
+// MEMORY instead of shared memory: K1t, an opt-in kernel of hqc_sparse_dense_mul_batch (HQC_S1_KERNEL=3),
+// and the product of the fused variant K4t (HQC_DEC_KERNEL=4). Same arithmetic as stage1.cuh
+// (r[W] ^= SHF(E[o + W], E[o + W + 1], s) for each support index, o = d >> 5, s = d & 31), different
+// load path.
+//
+// NOT CONSTANT-FLOW: the support is bucketed by offset range, so the trip count of each range's loop
+// (and whether a range ends with a single-index pass) depends on the secret y. The total arithmetic is
+// fixed, but the control flow is not (R#8, P:171 ask for execution independent of secret data), which
+// is why the library's defaults are the shared-memory kernels and these are opt-in.
 //
 // Why: the shared-memory kernels read one 32-bit word per (index, output word) pair and run at ~90% of
 // the 128 B/clk/SM shared-memory bound (profiles/r01b/NOTES.md, item 1); tcgen05.ld reads tensor memory
@@ -12,9 +18,8 @@
 // offset o, the window E[o + l R .. o + l R + R]. So row l holds a SKEWED copy of E:
 //     row l, column c  =  E[l R + t G + c]        c < COLS,  range t: o in [t G, t G + G),  G = COLS - R
 // and the index reads columns (o - t G) .. (o - t G) + R, all < COLS. The support indices are bucketed
-// by range (ballot compaction, fixed total count w: the instruction count does not depend on how the
-// indices fall into ranges), and for each range the warp refills its columns from E in shared memory
-// (conflict-free: lane stride R is odd) with tcgen05.st, then runs that range's indices.
+// by range (ballot compaction), and for each range the warp refills its columns from E in shared memory
+// (16-byte loads, see TmShape) with tcgen05.st, then runs that range's indices.
 // Shared-memory traffic per ciphertext drops from w * NW words (the windows) to NR * 32 * COLS (the
 // refills), HQC-3: 112,000 -> 49,152 words; the windows come from TMEM.
 //
