@@ -14,6 +14,6 @@ for L in 1 3 5; do
   timeout 300 $CMD > gpurun_out/prof_plain_L$L.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_decrypt -s 3 -c 1 -o gpurun_out/prof_fused_L$L $CMD > gpurun_out/ncu_fused_L$L.log 2>&1
 done
-for L in 3 5; do  # the tensor-memory standalone product (k_stage1t, the HQC-3/5 default of hqc_sparse_dense_mul_batch)
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stage1t -s 3 -c 1 -f -o gpurun_out/prof_s1t_L$L python scripts/time_s1_lib.py paper_2512_12904_b200/libhqcgpu.so $L > gpurun_out/ncu_s1t_L$L.log 2>&1
+for L in 3 5; do  # the opt-in tensor-memory standalone product (k_stage1t, HQC_S1_KERNEL=3)
+  HQC_S1_KERNEL=3 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stage1t -s 3 -c 1 -f -o gpurun_out/prof_s1t_L$L python scripts/time_s1_lib.py paper_2512_12904_b200/libhqcgpu.so $L > gpurun_out/ncu_s1t_L$L.log 2>&1
 done
