@@ -39,8 +39,13 @@ template <class P> constexpr int s1_unroll() {
 // One warp (NT = 32): su[Q0] and su[Q0 + 1] are first rewritten in place (su is a consumed staging row),
 // then each lane funnels a run of CH consecutive words (CH odd: conflict-free), loading every source
 // word once and carrying the neighbour in a register (no per-word selects). The warp pair (NT = 64)
-// keeps the strided form with per-word selects: two extra CTA barriers cost it more than the selects
-// (scripts/exp_build.py timings: HQC-1 -2% with the run form, HQC-3 +1.6%).
+// cannot afford the in-place fix-up (two more CTA barriers: +1.6% at HQC-3), so its runs stop before
+// the partial word Q0 and thread 0 adds the three words that involve it (no fix-up, no barrier: -0.5%
+// for the HQC-3 fused kernel, -0.2% for the HQC-5 standalone pair, against the strided form with
+// per-word selects; the one-warp kernels measured +0.4..0.5% with it and keep the in-place form).
+#ifndef HQC_EBUILD_RUN2
+#define HQC_EBUILD_RUN2 1
+#endif
 template <class P, class S, int NT = 32>
 __device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) {
   constexpr uint32_t NV = P::Q0 / 4;
@@ -50,7 +55,29 @@ __device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) 
   for (uint32_t c = lane; c < NV; c += NT)
     reinterpret_cast<uint4 *>(E)[c] = reinterpret_cast<const uint4 *>(su)[c];
   for (uint32_t q = 4 * NV + lane; q < P::Q0; q += NT) E[q] = su[q];
-  if constexpr (NT == 32) {
+  if constexpr (NT == 64 && HQC_EBUILD_RUN2) {
+    // Runs over x in [0, Q0 - 2], whose two source words are both below the partial word Q0 (no
+    // masking, no in-place fix-up, no barrier); thread 0 adds the three words that involve word Q0.
+    constexpr uint32_t NF = P::Q0 - 1;
+    constexpr uint32_t CH = ((NF + NT - 1) / NT) | 1u;  // per-thread run, odd: conflict-free
+    const uint32_t x0 = (uint32_t)lane * CH;
+    uint32_t lo = x0 < NF ? su[x0] : 0u;
+#pragma unroll 4
+    for (uint32_t t = 0; t < CH; t++) {
+      const uint32_t x = x0 + t;
+      if (x < NF) {
+        const uint32_t hi = su[x + 1];
+        E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+        lo = hi;
+      }
+    }
+    if (lane == 0) {
+      E[P::Q0] = eq0 | (su[0] << P::C);
+      E[2 * P::Q0] = __funnelshift_r(su[P::Q0 - 1], eq0, 32 - P::C);  // x = Q0 - 1
+      E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);         // x = Q0 (u32[Q0 + 1] = 0)
+    }
+    for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += NT) E[q] = 0u;
+  } else if constexpr (NT == 32) {
     constexpr uint32_t NF = P::Q0 + 1;                // funnel words x = 0..Q0
     constexpr uint32_t CH = ((NF + NT - 1) / NT) | 1u;  // per-lane run, odd
     const uint32_t s0 = su[0];
