@@ -84,8 +84,11 @@ const char *hqc_status_str(int status);
  *   v         [batch][v_words]  uint64   ciphertext part v (n1*n2 bits)
  *   y_support [batch][y_stride] uint32   the secret y's support, first w entries used (R#1)
  *   m_out     [batch][k]        uint8    decrypted messages (RS failure -> uncorrected bytes)
- * One kernel: stage 1 warp-per-ciphertext in shared memory, stage 2 lane-per-RM-block, stage 3
- * lane-per-ciphertext; no intermediate leaves the SM.
+ * One kernel: stage 1 in shared memory (a warp pair per ciphertext for HQC-3, one warp for
+ * HQC-1/5), stage 2 lane-per-RM-block, stage 3 lane-per-ciphertext; no intermediate leaves the SM.
+ * Constant-flow (R#8). HQC_DEC_KERNEL=1|2|3 forces the one-warp / pair / warp-specialised
+ * variant (same results); HQC_DEC_KERNEL=4 the tensor-memory-product variant, whose loop counts
+ * depend on y. The variable is read once per process.
  * ------------------------------------------------------------------------------------------- */
 int hqc_decrypt_batch(const hqc_params *p, const uint64_t *u, const uint64_t *v,
                       const uint32_t *y_support, uint8_t *m_out, size_t batch, void *stream);
