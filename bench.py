@@ -460,6 +460,31 @@ def standalone_product(args, dev, world, rank, hdist, hqc):
     return res
 
 
+def opt_in_variants():
+    """The opt-in tensor-memory kernels (not constant-flow, so not the library's defaults),
+    timed in subprocesses because the library reads its kernel switches once per process: the standalone
+    product with HQC_S1_KERNEL=3 (k_stage1t) and the fused decrypt with HQC_DEC_KERNEL=4 (k_decrypt_t), on
+    the same seeded inputs as the default lines (scripts/time_s1_lib.py, scripts/time_lib.py: 20 launches
+    after 3 warm-up launches, CUDA events)."""
+    import subprocess
+
+    root = os.path.dirname(os.path.abspath(__file__))
+    lib = os.path.join(root, "paper_2512_12904_b200", "libhqcgpu.so")
+    res = {"constant_flow": False}
+    for key, script, env_kv in (("standalone_product_k_stage1t_ms", "time_s1_lib.py", ("HQC_S1_KERNEL", "3")),
+                                ("fused_decrypt_k_decrypt_t_ms", "time_lib.py", ("HQC_DEC_KERNEL", "4"))):
+        env = dict(os.environ, **{env_kv[0]: env_kv[1]})
+        try:
+            r = subprocess.run([sys.executable, os.path.join(root, "scripts", script), lib, "1,3,5"], env=env,
+                               capture_output=True, text=True, timeout=300)
+            line = r.stdout.strip().splitlines()[-1]
+            res[key] = json.loads(line[line.index("{"):])
+        except Exception as e:  # a variant that cannot run is reported, not fatal for the bench line
+            res[key] = f"unavailable: {type(e).__name__}"
+    res["batch_per_gpu"] = 65536
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -473,6 +498,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=8192, help="ciphertexts per pipelined chunk of the host call")
     ap.add_argument("--no-levels", action="store_true", help="skip the per-level side measurements")
+    ap.add_argument("--no-variants", action="store_true", help="skip the opt-in tensor-memory kernel timings")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -629,6 +655,8 @@ def main():
         out["levels"] = side_levels(args, dev, world, rank, hdist, hqc, skip=args.level)
         out["standalone_product"] = standalone_product(args, dev, world, rank, hdist, hqc)
         out["next_rows"] = next_rows(args, dev, world, rank, hdist, hqc)
+    if rank == 0 and world == 1 and not args.no_levels and not args.no_variants:
+        out["opt_in_variants"] = opt_in_variants()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         got = hm.numpy().reshape(B, p.k)
         u = hu.numpy().view(np.uint64).reshape(B, -1)
