@@ -415,3 +415,60 @@ def test_edge_batches_new_entry_points():
     hqc.hqc_decrypt_ct_batch_host(level, torch.from_numpy(ct.reshape(-1)).pin_memory(), None, to_dev(W["y"]), hm, ws, 64)
     torch.cuda.synchronize()
     assert (hm.numpy() == W["m"][0]).all()
+
+
+def test_tensor_memory_variants_at_scale(tmp_path):
+    """The opt-in tensor-memory kernels at batches that make every warp loop: k_stage1t (HQC_S1_KERNEL=3)
+    over 5,000 products per level (more than 148 CTAs x 16 warps, so the grid-stride loop turns) and
+    k_decrypt_t (HQC_DEC_KERNEL=4) over 60,000 HQC-1 ciphertexts (34 per warp: two RS chunks). Their outputs
+    must equal the default constant-flow kernels' (themselves oracle-checked above) on the same seeded
+    random inputs; the switches are read once per process, so the variants run in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    arrs = {}
+    for level, B in ((1, 5000), (3, 5000), (5, 5000)):
+        p = oracle.params(level)
+        hp = hqc.params(level)
+        u = gen.dense(31, gen.TAG_U_RAND, 0, B, p.n, hp.u_stride)
+        v = gen.dense(31, gen.TAG_V_RAND, 0, B, p.n12, hp.v_words)
+        y = gen.support(31, gen.TAG_Y, 0, B, p.n, p.w, hp.y_stride)
+        r = torch.empty(B * hp.v_words * 8, dtype=torch.uint8, device=DEV)
+        hqc.hqc_sparse_dense_mul_batch(level, to_dev(u), to_dev(y), to_dev(v), r)
+        torch.cuda.synchronize()
+        arrs.update({f"u{level}": u, f"v{level}": v, f"y{level}": y, f"r{level}": r.cpu().numpy()})
+    B = 60000
+    p, hp = oracle.params(1), hqc.params(1)
+    u = gen.dense(32, gen.TAG_U_RAND, 0, B, p.n, hp.u_stride)
+    v = gen.dense(32, gen.TAG_V_RAND, 0, B, p.n12, hp.v_words)
+    y = gen.support(32, gen.TAG_Y, 0, B, p.n, p.w, hp.y_stride)
+    m = torch.empty(B * hp.k, dtype=torch.uint8, device=DEV)
+    hqc.hqc_decrypt_batch(1, to_dev(u), to_dev(v), to_dev(y), m)
+    torch.cuda.synchronize()
+    arrs.update({"du": u, "dv": v, "dy": y, "dm": m.cpu().numpy()})
+    f = tmp_path / "ref.npz"
+    np.savez(f, **arrs)
+    code = r'''
+import sys, numpy as np, torch
+from paper_2512_12904_b200 import hqc
+A = np.load(sys.argv[1])
+d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
+for level in (1, 3, 5):
+    hp = hqc.params(level)
+    B = A[f"u{level}"].shape[0]
+    r = torch.empty(B * hp.v_words * 8, dtype=torch.uint8, device="cuda")
+    hqc.hqc_sparse_dense_mul_batch(level, d(A[f"u{level}"]), d(A[f"y{level}"]), d(A[f"v{level}"]), r)
+    torch.cuda.synchronize()
+    assert (r.cpu().numpy() == A[f"r{level}"]).all(), ("k_stage1t", level)
+m = torch.empty(A["dm"].size, dtype=torch.uint8, device="cuda")
+hqc.hqc_decrypt_batch(1, d(A["du"]), d(A["dv"]), d(A["dy"]), m)
+torch.cuda.synchronize()
+assert (m.cpu().numpy() == A["dm"]).all(), "k_decrypt_t"
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HQC_S1_KERNEL="3", HQC_DEC_KERNEL="4")
+    r = subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
