@@ -640,6 +640,12 @@ template <class P> struct PairSmem {
   // XBUF: warp 1's accumulator image in its own buffer (after the barriers) instead of above r in E,
   // so warp 1 can store it without waiting for warp 0 to finish reading E (one CTA barrier fewer).
   static constexpr bool XBUF = HQC_PAIR_XBUF && !SPLIT_WORDS;
+#ifndef HQC_PAIR_RX
+#define HQC_PAIR_RX 1
+#endif
+  // RX: r is combined in place in XBUF and stage 2 reads it there, so the next ciphertext's E build
+  // does not have to wait for stage 2 (one CTA barrier fewer per ciphertext)
+  static constexpr bool RX = HQC_PAIR_RX && XBUF;
   static constexpr uint32_t XBUF_BYTES = XBUF ? round_up(P::NW * 4, 16) : 0;
   static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + D_BYTES + SYM_BYTES + 16 * 2 + XBUF_BYTES;
   static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // index split: warp 0 takes [0, W0), warp 1 [W0, W)
@@ -733,7 +739,7 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
           mbar_wait(bar, phase);
           phase ^= 1u;
         }
-        if (wid == 0) s1_store_r_xor2<S>(acc, E, xs, stg_v, lane);
+        if (wid == 0) s1_store_r_xor2<S>(acc, M::RX ? xs : E, xs, stg_v, lane);
       }
       __syncthreads();
       PHASE(4);
@@ -743,7 +749,8 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
 #endif
       if (!(HQC_EXP_SKIP & 1))
       for (uint32_t j = tid; j < P::N1; j += 64) {  // stage 2: one RM block per thread
-        const uint4 *src = reinterpret_cast<const uint4 *>(E) + j * (P::N2 / 128);
+        const uint4 *src = reinterpret_cast<const uint4 *>(M::RX ? reinterpret_cast<uint32_t *>(bar + 4) : E) +
+                           j * (P::N2 / 128);
         uint32_t X[P::MULT * 4];
 #pragma unroll
         for (int c = 0; c < (int)P::MULT; c++) {
@@ -753,7 +760,7 @@ __global__ void __launch_bounds__(64, DecOcc<P>::MIN_CTAS) k_decrypt(const uint6
         sym[j * M::SYM_PITCH + s] = (uint8_t)rm_decode_block<P::MULT>(X);
       }
       PHASE(5);
-      __syncthreads();
+      if (!M::RX) __syncthreads();  // (RX: the next E build writes E, not r; the barrier after it orders XBUF)
       PHASE(6);
     }
     for (uint32_t e = tid; e < P::N1 * 64; e += 64)
