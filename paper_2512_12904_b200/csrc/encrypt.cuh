@@ -244,8 +244,32 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
 // product, the encoders and the support XORs remain. CMP = true (KEM re-encryption check): each warp
 // compares its half of c' with the received c and writes its own flag, eq2_out[2 ct + warp]; the KDF
 // accepts iff both are set.
+#ifndef HQC_ENC_TAIL
+#define HQC_ENC_TAIL 1
+#endif
+// u = r1 + h*r2 needs all Q0 + 1 words of the ring element. When that one extra word over the n1*n2-bit
+// width raises the odd per-lane word count R (HQC-3: 1,121 words -> R = 37 instead of 35), the lanes
+// compute the first Q0 words and the warp adds word Q0 cooperatively (enc_tail_word): 5% fewer loads
+// and shifts for warp 0, which then matches warp 1's R (the pair runs in step).
+template <class P> constexpr uint32_t enc_tail() {
+  return (HQC_ENC_TAIL && make_odd_up((P::Q0 + 1 + 31) / 32) > make_odd_up((P::Q0 + 31) / 32)) ? 1u : 0u;
+}
+template <class P> using FullShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::WR>;
+
+// Word q of the product, whole warp: lane L takes indices L, L + 32, ... and the warp XOR-reduces.
+template <class P, class S>
+__device__ __forceinline__ uint32_t enc_tail_word(const uint32_t *E, const uint32_t *dsm, uint32_t q, int lane) {
+  uint32_t x = 0;
+  for (uint32_t j = lane; j < S::WT; j += 32) {
+    const uint32_t d = dsm[j];
+    const uint32_t *p = s1_window<P>(E + q, d);
+    x ^= __funnelshift_r(p[0], p[1], d);
+  }
+  return __reduce_xor_sync(0xffffffffu, x);
+}
+
 template <class P> struct Enc2Smem {
-  using SU = FullShape<P>;
+  using SU = FullShapeT<P>;
   using SV = EncVShape<P>;
   static constexpr uint32_t EU_BYTES = round_up(SU::E_WORDS * 4, 16);
   static constexpr uint32_t EV_BYTES = round_up(SV::E_WORDS * 4, 16);
@@ -308,6 +332,10 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
       s1_store_r<S>(acc, out, lane);
+      if constexpr (enc_tail<P>() != 0) {
+        const uint32_t t = enc_tail_word<P, S>(E, dsm, P::Q0, lane);
+        if (lane == 0) out[P::Q0] = t;
+      }
       __syncwarp();
       xor_support_bits(out, s_x, P::WR, P::N, lane);
       __syncwarp();
