@@ -90,8 +90,34 @@ __device__ __forceinline__ void copy_s2g(void *dst, const uint32_t *src, uint32_
   for (uint32_t c = lane; c < nwords / 4; c += 32) d[c] = reinterpret_cast<const uint4 *>(src)[c];
 }
 
-// One warp: out (NOUT words in smem, aliasing E) = dense (staged in su) * support (staged in ssup)
+#ifndef HQC_ENC_TAIL
+#define HQC_ENC_TAIL 1
+#endif
+// u = r1 + h*r2 needs all Q0 + 1 words of the ring element. When that one extra word over the n1*n2-bit
+// width raises the odd per-lane word count R (HQC-3: 1,121 words -> R = 37 instead of 35), the lanes
+// compute the first Q0 words and the warp adds word Q0 cooperatively (enc_tail_word): 5% fewer loads
+// and shifts for warp 0, which then matches warp 1's R (the pair runs in step).
+template <class P> constexpr uint32_t enc_tail() {
+  return (HQC_ENC_TAIL && make_odd_up((P::Q0 + 1 + 31) / 32) > make_odd_up((P::Q0 + 31) / 32)) ? 1u : 0u;
+}
+template <class P> using FullShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::WR>;
+template <class P> using KeyShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::W>;
+
+// Word q of the product, whole warp: lane L takes indices L, L + 32, ... and the warp XOR-reduces.
 template <class P, class S>
+__device__ __forceinline__ uint32_t enc_tail_word(const uint32_t *E, const uint32_t *dsm, uint32_t q, int lane) {
+  uint32_t x = 0;
+  for (uint32_t j = lane; j < S::WT; j += 32) {
+    const uint32_t d = dsm[j];
+    const uint32_t *p = s1_window<P>(E + q, d);
+    x ^= __funnelshift_r(p[0], p[1], d);
+  }
+  return __reduce_xor_sync(0xffffffffu, x);
+}
+
+// One warp: out (NOUT words in smem, aliasing E) = dense (staged in su) * support (staged in ssup);
+// TAIL: also word NOUT (= Q0), computed by the whole warp before r overwrites E (see enc_tail).
+template <class P, class S, bool TAIL = false>
 __device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
                                              int lane) {
   s1_stage_d<P, S>(ssup, dsm, lane);
@@ -99,8 +125,13 @@ __device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup,
   __syncwarp();
   uint32_t acc[S::R];
   s1_product<P, S>(E, dsm, acc, lane);
+  uint32_t t = 0;
+  if constexpr (TAIL) t = enc_tail_word<P, S>(E, dsm, S::NOUT, lane);
   __syncwarp();
   s1_store_r<S>(acc, E, lane);
+  if constexpr (TAIL) {
+    if (lane == 0) E[S::NOUT] = t;
+  }
   __syncwarp();
 }
 
@@ -130,7 +161,7 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
                                                const uint32_t *__restrict__ y, uint64_t *__restrict__ s, size_t nkeys) {
   extern __shared__ __align__(16) uint8_t smem[];
   using M = EncSmem<P>;
-  using S = KeyShape<P>;
+  using S = KeyShapeT<P>;
   const int lane = threadIdx.x;
   uint32_t *E = reinterpret_cast<uint32_t *>(smem);
   uint32_t *stg = reinterpret_cast<uint32_t *>(smem + M::E_BYTES);
@@ -142,7 +173,7 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
     copy_g2s(sx, x + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     copy_g2s(sy, y + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     __syncwarp();
-    warp_product<P, S>(stg, sy, E, dsm, lane);
+    warp_product<P, S, enc_tail<P>() != 0>(stg, sy, E, dsm, lane);
     xor_support_bits(E, sx, P::W, P::N, lane);
     __syncwarp();
     if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;  // bits >= n are zero
@@ -244,30 +275,6 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
 // product, the encoders and the support XORs remain. CMP = true (KEM re-encryption check): each warp
 // compares its half of c' with the received c and writes its own flag, eq2_out[2 ct + warp]; the KDF
 // accepts iff both are set.
-#ifndef HQC_ENC_TAIL
-#define HQC_ENC_TAIL 1
-#endif
-// u = r1 + h*r2 needs all Q0 + 1 words of the ring element. When that one extra word over the n1*n2-bit
-// width raises the odd per-lane word count R (HQC-3: 1,121 words -> R = 37 instead of 35), the lanes
-// compute the first Q0 words and the warp adds word Q0 cooperatively (enc_tail_word): 5% fewer loads
-// and shifts for warp 0, which then matches warp 1's R (the pair runs in step).
-template <class P> constexpr uint32_t enc_tail() {
-  return (HQC_ENC_TAIL && make_odd_up((P::Q0 + 1 + 31) / 32) > make_odd_up((P::Q0 + 31) / 32)) ? 1u : 0u;
-}
-template <class P> using FullShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::WR>;
-
-// Word q of the product, whole warp: lane L takes indices L, L + 32, ... and the warp XOR-reduces.
-template <class P, class S>
-__device__ __forceinline__ uint32_t enc_tail_word(const uint32_t *E, const uint32_t *dsm, uint32_t q, int lane) {
-  uint32_t x = 0;
-  for (uint32_t j = lane; j < S::WT; j += 32) {
-    const uint32_t d = dsm[j];
-    const uint32_t *p = s1_window<P>(E + q, d);
-    x ^= __funnelshift_r(p[0], p[1], d);
-  }
-  return __reduce_xor_sync(0xffffffffu, x);
-}
-
 template <class P> struct Enc2Smem {
   using SU = FullShapeT<P>;
   using SV = EncVShape<P>;
