@@ -110,20 +110,31 @@ template <class P> struct S1Pipe {
   __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane, uint32_t *rout = nullptr) {
     if (rout == nullptr) rout = E;
     wait();
-    using S = DecShape<P>;
+    using S = DecShape<P>;    // E and the staged rows
+    using ST = DecShapeT<P>;  // the lanes' product; words [ST::NOUT, NW) by s1_tail_words
+    constexpr uint32_t TW = dec_tail_words<P>();
     s1_stage_d<P, S>(stg_y, dsm, lane);
     s1_build_E<P, S>(stg_u, E, lane);
     __syncwarp();
     if (v) issue_v(ct, lane);
     else if (has_next) issue_uy(next, lane);  // no v to stage: the next rows land during this product
-    uint32_t acc[S::R];
-    s1_product<P, S>(E, dsm, acc, lane);
+    uint32_t acc[ST::R];
+    s1_product<P, ST>(E, dsm, acc, lane);
+    uint32_t mine = 0;  // lane i < TW: word ST::NOUT + i
+    if constexpr (TW > 0) {
+      uint32_t t[TW];
+      s1_tail_words<P, ST, ST::NOUT, TW>(E, dsm, lane, t);
+#pragma unroll
+      for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
+    }
     __syncwarp();  // every lane is done reading E: r overwrites it
     if (v) {
       wait();  // v has landed in the staging buffer during the product loop
-      s1_store_r_xor<S>(acc, rout, stg_u, lane);
+      s1_store_r_xor<ST>(acc, rout, stg_u, lane);
+      if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine ^ stg_u[ST::NOUT + lane];
     } else {
-      s1_store_r<S>(acc, rout, lane);
+      s1_store_r<ST>(acc, rout, lane);
+      if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine;
     }
     __syncwarp();
     if (v && has_next) issue_uy(next, lane);

@@ -48,6 +48,17 @@ template <class P, uint32_t NOUT_, uint32_t WT_> struct ProdShape {
   static constexpr uint32_t WPAD = round_up(WT, 4);
 };
 template <class P> using DecShape = ProdShape<P, P::NW, P::W>;          // u*y truncated to n1*n2 bits
+// The one-warp decrypt product without the ragged top: the largest odd R with 32 R <= NW words per warp,
+// the remaining TW = NW - 32 R words (HQC-1: 552 = 32 * 17 + 8) added by the whole warp (s1_tail_words);
+// TW = 0 where NW is already 32 x odd (HQC-3) or the rest would be too wide (HQC-5: 40 words).
+#ifndef HQC_S1_TAILW
+#define HQC_S1_TAILW 1
+#endif
+template <class P> constexpr uint32_t dec_tail_words() {
+  constexpr uint32_t r = ((P::NW / 32) & 1u) ? P::NW / 32 : P::NW / 32 - 1;  // largest odd, 32 r <= NW
+  return (HQC_S1_TAILW && P::NW - 32 * r > 0 && P::NW - 32 * r <= 8) ? P::NW - 32 * r : 0u;
+}
+template <class P> using DecShapeT = ProdShape<P, P::NW - dec_tail_words<P>(), P::W>;
 template <class P> using FullShape = ProdShape<P, P::Q0 + 1, P::WR>;    // h*r2: all n bits
 template <class P> using KeyShape = ProdShape<P, P::Q0 + 1, P::W>;      // h*y: all n bits
 template <class P> using EncVShape = ProdShape<P, P::NW, P::WR>;        // s*r2 truncated

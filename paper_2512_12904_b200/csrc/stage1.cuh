@@ -183,6 +183,29 @@ __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *ds
   s1_product_range<P, S>(E, dsm, acc, lane, 0, S::WT);
 }
 
+// Words [Q, Q + TW) of the product by the whole warp (the ragged top above the lanes' R-word blocks): lane
+// L takes support indices L, L + 32, ... (a fixed count per level), funnels TW + 1 consecutive words of
+// each window, and the warp XOR-reduces each word (REDUX). Reads E: call before r overwrites it.
+template <class P, class S, uint32_t Q, uint32_t TW>
+__device__ __forceinline__ void s1_tail_words(const uint32_t *E, const uint32_t *dsm, int lane, uint32_t (&t)[TW]) {
+  uint32_t x[TW];
+#pragma unroll
+  for (uint32_t i = 0; i < TW; i++) x[i] = 0;
+  for (uint32_t j = lane; j < S::WT; j += 32) {
+    const uint32_t d = dsm[j];
+    const uint32_t *p = s1_window<P>(E + Q, d);
+    uint32_t a = p[0];
+#pragma unroll
+    for (uint32_t i = 0; i < TW; i++) {
+      const uint32_t b = p[i + 1];
+      x[i] ^= __funnelshift_r(a, b, d);
+      a = b;
+    }
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < TW; i++) t[i] = __reduce_xor_sync(0xffffffffu, x[i]);
+}
+
 // Store the accumulators (S::NOUT words, aliasing E). The caller synchronises the warp first.
 template <class S>
 __device__ __forceinline__ void s1_store_r(const uint32_t (&acc)[S::R], uint32_t *rsm, int lane) {
