@@ -93,31 +93,32 @@ __device__ __forceinline__ void copy_s2g(void *dst, const uint32_t *src, uint32_
 #ifndef HQC_ENC_TAIL
 #define HQC_ENC_TAIL 1
 #endif
-// u = r1 + h*r2 needs all Q0 + 1 words of the ring element. When that one extra word over the n1*n2-bit
-// width raises the odd per-lane word count R (HQC-3: 1,121 words -> R = 37 instead of 35), the lanes
-// compute the first Q0 words and the warp adds word Q0 cooperatively (enc_tail_word): 5% fewer loads
-// and shifts for warp 0, which then matches warp 1's R (the pair runs in step).
-template <class P> constexpr uint32_t enc_tail() {
-  return (HQC_ENC_TAIL && make_odd_up((P::Q0 + 1 + 31) / 32) > make_odd_up((P::Q0 + 31) / 32)) ? 1u : 0u;
+// A product over NTOT words whose odd per-lane word count R = odd ceil(NTOT / 32) wastes slots (HQC-1: 552
+// / 553 words -> R = 19; HQC-3's u: 1,121 words -> R = 37) runs with the largest odd R such that 32 R <=
+// NTOT, and the warp adds the TW <= 9 words above 32 R cooperatively (s1_tail_words: lane-strided support
+// indices, one REDUX.XOR per word). HQC-5's tops (40+ words) keep the plain shape.
+template <uint32_t NTOT> constexpr uint32_t enc_tail_words() {
+  constexpr uint32_t r = ((NTOT / 32) & 1u) ? NTOT / 32 : NTOT / 32 - 1;
+  return (HQC_ENC_TAIL && NTOT - 32 * r > 0 && NTOT - 32 * r <= 9) ? NTOT - 32 * r : 0u;
 }
+template <class P> constexpr uint32_t enc_tail() { return enc_tail_words<P::Q0 + 1>(); }       // u, s
+template <class P> constexpr uint32_t enc_tail_v() { return enc_tail_words<P::NW>(); }         // v
 template <class P> using FullShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::WR>;
 template <class P> using KeyShapeT = ProdShape<P, P::Q0 + 1 - enc_tail<P>(), P::W>;
+template <class P> using EncVShapeT = ProdShape<P, P::NW - enc_tail_v<P>(), P::WR>;
 
-// Word q of the product, whole warp: lane L takes indices L, L + 32, ... and the warp XOR-reduces.
-template <class P, class S>
-__device__ __forceinline__ uint32_t enc_tail_word(const uint32_t *E, const uint32_t *dsm, uint32_t q, int lane) {
-  uint32_t x = 0;
-  for (uint32_t j = lane; j < S::WT; j += 32) {
-    const uint32_t d = dsm[j];
-    const uint32_t *p = s1_window<P>(E + q, d);
-    x ^= __funnelshift_r(p[0], p[1], d);
-  }
-  return __reduce_xor_sync(0xffffffffu, x);
+// Store words [S::NOUT, S::NOUT + TW) of the tail (t: every lane holds all TW values) into out.
+template <class S, uint32_t TW>
+__device__ __forceinline__ void store_tail(const uint32_t (&t)[TW], uint32_t *out, int lane) {
+  uint32_t mine = 0;
+#pragma unroll
+  for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
+  if ((uint32_t)lane < TW) out[S::NOUT + lane] = mine;
 }
 
-// One warp: out (NOUT words in smem, aliasing E) = dense (staged in su) * support (staged in ssup);
-// TAIL: also word NOUT (= Q0), computed by the whole warp before r overwrites E (see enc_tail).
-template <class P, class S, bool TAIL = false>
+// One warp: out (NOUT + TW words in smem, aliasing E) = dense (staged in su) * support (staged in ssup);
+// the TW top words are computed by the whole warp before r overwrites E.
+template <class P, class S, uint32_t TW = 0>
 __device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
                                              int lane) {
   s1_stage_d<P, S>(ssup, dsm, lane);
@@ -125,13 +126,11 @@ __device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup,
   __syncwarp();
   uint32_t acc[S::R];
   s1_product<P, S>(E, dsm, acc, lane);
-  uint32_t t = 0;
-  if constexpr (TAIL) t = enc_tail_word<P, S>(E, dsm, S::NOUT, lane);
+  uint32_t t[TW > 0 ? TW : 1];
+  if constexpr (TW > 0) s1_tail_words<P, S, S::NOUT, TW>(E, dsm, lane, t);
   __syncwarp();
   s1_store_r<S>(acc, E, lane);
-  if constexpr (TAIL) {
-    if (lane == 0) E[S::NOUT] = t;
-  }
+  if constexpr (TW > 0) store_tail<S, TW>(t, E, lane);
   __syncwarp();
 }
 
@@ -173,7 +172,7 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
     copy_g2s(sx, x + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     copy_g2s(sy, y + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     __syncwarp();
-    warp_product<P, S, enc_tail<P>() != 0>(stg, sy, E, dsm, lane);
+    warp_product<P, S, enc_tail<P>()>(stg, sy, E, dsm, lane);
     xor_support_bits(E, sx, P::W, P::N, lane);
     __syncwarp();
     if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;  // bits >= n are zero
@@ -277,7 +276,7 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
 // accepts iff both are set.
 template <class P> struct Enc2Smem {
   using SU = FullShapeT<P>;
-  using SV = EncVShape<P>;
+  using SV = EncVShapeT<P>;
   static constexpr uint32_t EU_BYTES = round_up(SU::E_WORDS * 4, 16);
   static constexpr uint32_t EV_BYTES = round_up(SV::E_WORDS * 4, 16);
   // staging of a key row (2 u_stride words), then the warp's product output
@@ -340,8 +339,9 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       s1_product<P, S>(E, dsm, acc, lane);
       s1_store_r<S>(acc, out, lane);
       if constexpr (enc_tail<P>() != 0) {
-        const uint32_t t = enc_tail_word<P, S>(E, dsm, P::Q0, lane);
-        if (lane == 0) out[P::Q0] = t;
+        uint32_t t[enc_tail<P>()];
+        s1_tail_words<P, S, S::NOUT, enc_tail<P>()>(E, dsm, lane, t);
+        store_tail<S, enc_tail<P>()>(t, out, lane);
       }
       __syncwarp();
       xor_support_bits(out, s_x, P::WR, P::N, lane);
@@ -366,6 +366,11 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
       s1_store_r<S>(acc, out, lane);
+      if constexpr (enc_tail_v<P>() != 0) {
+        uint32_t t[enc_tail_v<P>()];
+        s1_tail_words<P, S, S::NOUT, enc_tail_v<P>()>(E, dsm, lane, t);
+        store_tail<S, enc_tail_v<P>()>(t, out, lane);
+      }
       __syncwarp();
       for (uint32_t j = lane; j < P::N1; j += 32) {  // RM-encode symbol j into block j, every copy
         uint32_t w[4];

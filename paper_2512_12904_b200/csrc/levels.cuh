@@ -44,7 +44,9 @@ template <int LEVEL> struct Lv : Table1<LEVEL> {
 template <class P, uint32_t NOUT_, uint32_t WT_> struct ProdShape {
   static constexpr uint32_t NOUT = NOUT_, WT = WT_;
   static constexpr uint32_t R = make_odd_up((NOUT + 31) / 32);
-  static constexpr uint32_t E_WORDS = round_up(P::Q0 + 32 * R + 2, 4);
+  // at least the doubled u (2 Q0 + 2 words, which s1_build_E always writes) for the narrow-R shapes
+  static constexpr uint32_t E_WORDS = round_up(P::Q0 + 32 * R + 2 > 2 * P::Q0 + 2 ? P::Q0 + 32 * R + 2
+                                                                                  : 2 * P::Q0 + 2, 4);
   static constexpr uint32_t WPAD = round_up(WT, 4);
 };
 template <class P> using DecShape = ProdShape<P, P::NW, P::W>;          // u*y truncated to n1*n2 bits
