@@ -24,6 +24,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "HQC-1/3/5 PKE decryptions/sec per B200 and 8xB200; fraction of roofline"
 CONFIG_SEED = {1: 0xC0F1_0001, 3: 0xC0F1_0002, 5: 0xC0F1_0003}
+ADV_SEED = 0xC0F1_0004  # BASELINE configs[3] (tests/workloads.py CONFIG_SEED[4])
 WORKLOAD = {1: "configs[0]-shape HQC-1 PKE decrypt", 3: "configs[1] HQC-3 PKE decrypt, batch 65536/GPU",
             5: "configs[2] HQC-5 PKE decrypt"}
 
@@ -185,7 +186,7 @@ def gen_shape(p):
                      v_words=p.v_words, y_stride=p.y_stride, sup_stride=p.e_stride)
 
 
-def make_valid_workload(level: int, i0: int, B: int, p, dev, chunk: int = 1 << 18):
+def make_valid_workload(level: int, i0: int, B: int, p, dev, chunk: int = 1 << 18, seed: int | None = None):
     """Valid ciphertexts for BASELINE configs[0..2] built on the device: the seeded
     generator draws keys (h, x, y; one keypair per 256 ciphertexts) and per-ciphertext (m, r1, r2, e)
     on the host; the library's keygen/encrypt kernels produce s, u, v.
@@ -194,7 +195,7 @@ def make_valid_workload(level: int, i0: int, B: int, p, dev, chunk: int = 1 << 1
 
     from paper_2512_12904_b200 import gen, hqc
 
-    seed = CONFIG_SEED[level]
+    seed = CONFIG_SEED[level] if seed is None else seed
     sh = gen_shape(p)
     key = gen.key_of(i0, B)
     k0, nk = int(key[0]), int(key[-1] - key[0] + 1)
@@ -273,7 +274,7 @@ def run_reference(args):
 
     op = oracle.params(args.level)
     cores = os.cpu_count() or 1
-    per_step = max(cores * 8, 64)
+    per_step = max(4096, cores * 256)  # the same order of sample per thread as the cpu_baseline leg
     sh = gen.Shape(n=op.n, w=op.w, wr=op.wr, n1=op.n1, k=op.k, n2=op.n2, delta=op.delta,
                    u_stride=op.words + (op.words & 1), v_words=op.vwords, y_stride=(op.w + 3) // 4 * 4,
                    sup_stride=(op.wr + 3) // 4 * 4)
@@ -286,7 +287,7 @@ def run_reference(args):
     u, v = oracle.encrypt_batch(op, h, s, key, m, r1, r2, e, nthreads=cores)
     yy = np.ascontiguousarray(y[key])
     for _ in range(args.warmup):
-        oracle.decrypt_batch(op, u[:cores], v[:cores], yy[:cores], nthreads=cores)
+        oracle.decrypt_batch(op, u, v, yy, nthreads=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         got = oracle.decrypt_batch(op, u, v, yy, nthreads=cores)
@@ -485,6 +486,175 @@ def opt_in_variants():
     return res
 
 
+def _alu_peak(dev) -> float:
+    """ALU-pipe peak per GPU in int-ops/s: 64 lanes/clk/SM (K7-measured 63.7) x SMs x sm_max_mhz."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    return 64 * sms * float(measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
+
+
+def _timed_ms(fn, steps: int) -> float:
+    """Mean device time of fn() over `steps` back-to-back calls, CUDA events on the current stream."""
+    import torch
+
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def config1_block(args, dev, world, rank, hdist, hqc, B: int = 1024) -> dict:
+    """BASELINE configs[0]: HQC-1, batch 1,024 per GPU (valid ciphertexts). Two numbers (SURVEY §7,
+    PAPER.md:237 repeated runs): the steady-state rate of back-to-back launches captured in one CUDA Graph
+    (launch overhead amortised), and the latency of ONE launch (CUDA events around a single launch on an
+    idle GPU, median of 50), plus the host-side wall time of launch + synchronize."""
+    import torch
+
+    level = 1
+    p = hqc.params(level)
+    du, dv, dy, dref = make_valid_workload(level, rank * B, B, p, dev)
+    dm = torch.empty(B * p.k, dtype=torch.uint8, device=dev)
+    run = lambda: hqc.hqc_decrypt_batch(level, du, dv, dy, dm)  # noqa: E731
+    for _ in range(5):
+        run()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    lat, wall = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(50):
+        t0 = time.perf_counter()
+        e0.record(st)
+        run()
+        e1.record(st)
+        e1.synchronize()
+        wall.append(time.perf_counter() - t0)
+        lat.append(e0.elapsed_time(e1))
+    G, R = 64, 10
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(G):
+            run()
+    for _ in range(3):
+        g.replay()
+    ms_graph = _timed_ms(g.replay, R) / G
+    ms_stream = _timed_ms(run, G)  # plain back-to-back launches on the stream (no graph)
+    ms = hdist.max_over_ranks(ms_graph, dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    hqc.hqc_count_mismatch(level, dm, dref, cnt)
+    ops = algorithmic_ops(p)["total"]
+    val = world * B / (ms / 1e3)
+    grid, wpc = hqc.hqc_decrypt_launch_shape(level, B)
+    return {"workload": "configs[0] HQC-1 PKE decrypt, batch 1024/GPU", "batch_per_gpu": B,
+            "value": val, "unit": "decryptions/s", "graph_ms_per_launch": ms, "graph_launches": G * R,
+            "alu_roofline_frac": val / world * ops / _alu_peak(dev),
+            "stream_ms_per_launch": hdist.max_over_ranks(ms_stream, dev),
+            "single_launch_ms": {"median": float(np.median(lat)), "min": float(min(lat)), "n": len(lat)},
+            "single_launch_host_wall_ms": {"median": 1e3 * float(np.median(wall)), "min": 1e3 * float(min(wall))},
+            "launch": {"grid": grid, "warps_per_cta": wpc},
+            "mismatches_vs_message": hdist.sum_over_ranks(cnt)}
+
+
+def config4_block(args, dev, world, rank, hdist, hqc, total: int = 1 << 20) -> dict:
+    """BASELINE configs[3]: HQC-1 adversarial decrypt, 1,048,576 ciphertexts in four quarters (DESIGN.md §5,
+    R#17), split evenly over the ranks: Q0 valid; Q1 valid with delta RM blocks of v randomised; Q2 with
+    delta+1..2 delta blocks randomised; Q3 uniformly random u and v with the key's y. The valid ciphertexts
+    are built on the device (generator draws -> GPU encrypt), the block patches and the Q3 rows come from
+    the same seeded generator as tests/workloads.adversarial_batch (bit-identical inputs; the full-size
+    oracle comparison is tests/test_gpu_config4.py). Timed like the headline; the decrypt is constant-flow,
+    so the garbage quarters cost the same as the valid one."""
+    import torch
+
+    from paper_2512_12904_b200 import gen
+
+    level = 1
+    p = hqc.params(level)
+    sh = gen_shape(p)
+    i0, n = hdist.split_even(total, world, rank)
+    du, dv, dy, dref = make_valid_workload(level, i0, n, p, dev, seed=ADV_SEED)
+    q = gen.quarter_of(np.arange(i0, i0 + n), total)
+    bw = p.n2 // 64
+    v3 = dv.view(torch.int64).view(n, p.n1, bw)
+    for quarter, (tmin, tmax) in ((1, (p.delta, p.delta)), (2, (p.delta + 1, 2 * p.delta))):
+        mask = q == quarter
+        if mask.any():
+            _, patches = gen.block_patches(i0, n, ADV_SEED + quarter, sh, tmin, tmax, row_mask=mask)
+            for rr, b, bits in patches:
+                v3[torch.from_numpy(rr).to(dev), torch.from_numpy(b).to(dev)] = torch.from_numpy(
+                    bits.view(np.int64)).to(dev)
+    idx = np.nonzero(q == 3)[0]
+    if idx.size:
+        j0, cnt = int(idx[0]), int(idx.size)
+        for c0 in range(0, cnt, 1 << 17):
+            c = min(1 << 17, cnt - c0)
+            uu = gen.dense(ADV_SEED, gen.TAG_U_RAND, i0 + j0 + c0, c, p.n, p.u_stride)
+            vv = gen.dense(ADV_SEED, gen.TAG_V_RAND, i0 + j0 + c0, c, p.n12, p.v_words)
+            du.view(n, -1)[j0 + c0:j0 + c0 + c] = torch.from_numpy(uu.view(np.uint8)).to(dev)
+            dv.view(n, -1)[j0 + c0:j0 + c0 + c] = torch.from_numpy(vv.view(np.uint8)).to(dev)
+    dm = torch.empty(n * p.k, dtype=torch.uint8, device=dev)
+    run = lambda: hqc.hqc_decrypt_batch(level, du, dv, dy, dm)  # noqa: E731
+    for _ in range(3):
+        run()
+    ms = hdist.max_over_ranks(_timed_ms(run, max(5, args.steps // 4)), dev)
+    eq = (dm.view(n, p.k) == dref.view(n, p.k)).all(dim=1).cpu().numpy()
+    per_q = {}
+    for quarter in range(4):
+        sel = q == quarter
+        per_q[f"Q{quarter}"] = [hdist.sum_over_ranks(int(eq[sel].sum()), dev), hdist.sum_over_ranks(int(sel.sum()), dev)]
+    val = total / (ms / 1e3)
+    ops = algorithmic_ops(p)["total"]
+    out = {"workload": "configs[3] HQC-1 adversarial decrypt, batch 1048576 (split over GPUs)", "total_batch": total,
+           "value": val, "unit": "decryptions/s", "ms_per_step": ms,
+           "alu_roofline_frac": val / world * ops / _alu_peak(dev),
+           "outputs_equal_message_per_quarter": per_q,
+           "q0_mismatches_vs_message": per_q["Q0"][1] - per_q["Q0"][0],
+           "parity": "all 1,048,576 rows vs the oracle: tests/test_gpu_config4.py (-m gpu)"}
+    del du, dv, dy, dref, dm, v3
+    torch.cuda.empty_cache()
+    return out
+
+
+def config5_block(args, dev, world, rank, hdist, hqc, total: int = 4_194_304) -> dict:
+    """BASELINE configs[4]: HQC-1, HQC-3 and HQC-5 each at 4,194,304 valid ciphertexts, split evenly and
+    contiguously over the N ranks (hdist.split_even: strong scaling; per-index seeding, so the bytes are the
+    same for every N). Per level: K launches of this rank's shard between CUDA events, MAX over ranks; the
+    mismatch count vs the generator's messages is SUMmed over NCCL; clocks are sampled on every rank during
+    its timed region (hdist.scaling_run, the function the gloo test drives)."""
+    import torch
+
+    steps = max(3, args.steps // 8)
+
+    def run_shard(level, i0, n):
+        p = hqc.params(level)
+        du, dv, dy, dref = make_valid_workload(level, i0, n, p, dev)
+        dm = torch.empty(n * p.k, dtype=torch.uint8, device=dev)
+        run = lambda: hqc.hqc_decrypt_batch(level, du, dv, dy, dm)  # noqa: E731
+        run()
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        with ClockSampler(dev) as clk:
+            ms = _timed_ms(run, steps)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        hqc.hqc_count_mismatch(level, dm, dref, cnt)
+        bad = int(cnt.item())
+        del du, dv, dy, dref, dm
+        torch.cuda.empty_cache()
+        return ms, bad, clk.summary()
+
+    ops = {lv: algorithmic_ops(hqc.params(lv))["total"] for lv in (1, 3, 5)}
+    res = hdist.scaling_run((1, 3, 5), total, world, rank, run_shard, ops, _alu_peak(dev), dev)
+    return {"workload": "configs[4] HQC-1/3/5 PKE decrypt, 4194304 each, split evenly over the GPUs",
+            "scaling": "strong", "steps": steps, "levels": res}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -499,6 +669,8 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=8192, help="ciphertexts per pipelined chunk of the host call")
     ap.add_argument("--no-levels", action="store_true", help="skip the per-level side measurements")
     ap.add_argument("--no-variants", action="store_true", help="skip the opt-in tensor-memory kernel timings")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs[0]/[3]/[4] blocks")
+    ap.add_argument("--config5-total", type=int, default=4_194_304, help="ciphertexts per level in configs[4]")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -513,6 +685,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's INIT lines (communicator size, ranks, transports) go to the log, so the run shows that NCCL
+        # saw all N ranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     p = hqc.params(args.level)
     B = args.batch
@@ -617,7 +793,7 @@ def main():
 
     ops = algorithmic_ops(p)
     peaks = measured_peaks()
-    c = clk.summary()
+    c = hdist.merge_clocks(hdist.gather_objects(clk.summary()))  # every rank's clocks: min / union
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     kernel_s = ms / 1e3 / args.steps
@@ -650,13 +826,25 @@ def main():
                                  "grid": gw[0], "warps_per_cta": gw[1]}},
            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
            "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"],
-                      "samples": c["samples"], "source": "NVML, 2 ms period, timed region only"}}
+                      "samples": c["samples"], "sm_mhz_min": c["sm_mhz_min"],
+                      "per_rank_sm_mhz": c["per_rank_sm_mhz"],
+                      "source": "NVML on every rank, 2 ms period, timed region only; sm_mhz = slowest rank's median, "
+                                "reasons = union over ranks"}}
+    # the wide tables first; the per-config / per-level headline blocks LAST in the line (they are what a
+    # reader of the log's tail needs)
+    tail = {}
     if not args.no_levels:
-        out["levels"] = side_levels(args, dev, world, rank, hdist, hqc, skip=args.level)
-        out["standalone_product"] = standalone_product(args, dev, world, rank, hdist, hqc)
         out["next_rows"] = next_rows(args, dev, world, rank, hdist, hqc)
     if rank == 0 and world == 1 and not args.no_levels and not args.no_variants:
         out["opt_in_variants"] = opt_in_variants()
+    if not args.no_configs:
+        tail["config1"] = config1_block(args, dev, world, rank, hdist, hqc)
+        tail["config4"] = config4_block(args, dev, world, rank, hdist, hqc)
+    if not args.no_levels:
+        tail["standalone_product"] = standalone_product(args, dev, world, rank, hdist, hqc)
+        tail["levels"] = side_levels(args, dev, world, rank, hdist, hqc, skip=args.level)
+    if not args.no_configs:
+        tail["config5"] = config5_block(args, dev, world, rank, hdist, hqc, args.config5_total)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         got = hm.numpy().reshape(B, p.k)
         u = hu.numpy().view(np.uint64).reshape(B, -1)
@@ -664,6 +852,7 @@ def main():
         y = hy.numpy().view(np.uint32).reshape(B, -1)
         m_ref = dref.cpu().numpy().reshape(B, p.k) if dref is not None else None
         out["cpu_baseline"] = cpu_baseline(args.level, u, v, y, got, m_ref)
+    out.update(tail)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -49,3 +49,51 @@ def sum_over_ranks(count, device=None) -> int:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
+
+
+def gather_objects(obj) -> list:
+    """Every rank's `obj` (picklable), in rank order; [obj] for a single process."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def merge_clocks(per_rank: list) -> dict:
+    """Clock records of all ranks (each {"sm_mhz", "sm_mhz_min", "sm_max_mhz", "reasons", "samples"}) ->
+    one record: the median SM clock of the slowest rank, the minimum over ranks, the union of the
+    throttle reasons, and the per-rank medians (a throttled rank is visible, not averaged away)."""
+    med = [c.get("sm_mhz") for c in per_rank if c.get("sm_mhz") is not None]
+    mins = [c.get("sm_mhz_min", c.get("sm_mhz")) for c in per_rank if c.get("sm_mhz") is not None]
+    reasons = sorted({r for c in per_rank for r in c.get("reasons", [])})
+    maxes = [c.get("sm_max_mhz") for c in per_rank if c.get("sm_max_mhz") is not None]
+    return {"sm_mhz": min(med) if med else None, "sm_mhz_min": min(mins) if mins else None,
+            "sm_max_mhz": max(maxes) if maxes else None, "reasons": reasons,
+            "samples": sum(int(c.get("samples", 0)) for c in per_rank),
+            "per_rank_sm_mhz": [c.get("sm_mhz") for c in per_rank]}
+
+
+def scaling_run(levels, total: int, world: int, rank: int, run_shard, ops_per_unit: dict, peak_per_gpu: float,
+                device=None) -> dict:
+    """Strong-scaling measurement of BASELINE configs[4]: for each level, `total` units split
+    evenly and contiguously over the ranks (split_even); run_shard(level, i0, n) runs this rank's shard
+    and returns (ms_per_step, mismatches, clocks); the job's time is the MAX over ranks, the mismatches the
+    SUM, the clocks are gathered from every rank. The same function runs under gloo in the CPU tests."""
+    res = {}
+    for level in levels:
+        i0, n = split_even(total, world, rank)
+        ms, bad, clk = run_shard(level, i0, n)
+        ms_max = max_over_ranks(ms, device)
+        bad_sum = sum_over_ranks(int(bad), device)
+        clocks = merge_clocks(gather_objects(clk))
+        shards = gather_objects((i0, n))
+        val = total / (ms_max / 1e3)
+        res[str(level)] = {"value": val, "unit": "decryptions/s", "total_batch": total, "n_gpus": world,
+                           "ms_per_step": ms_max, "per_gpu_value": val / world,
+                           "alu_roofline_frac": val / world * ops_per_unit[level] / peak_per_gpu,
+                           "mismatches_vs_message": bad_sum, "shards": [list(s) for s in shards],
+                           "clocks": clocks}
+    return res

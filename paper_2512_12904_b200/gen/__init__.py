@@ -133,12 +133,9 @@ def quarter_of(i: np.ndarray, batch: int) -> np.ndarray:
     return np.minimum(np.asarray(i) // max(q, 1), 3)
 
 
-def randomise_blocks(v: np.ndarray, i0: int, seed: int, sh: Shape, tmin: int, tmax: int, row_mask=None,
-                     nthreads=None):
-    """Overwrite t ~ U{tmin..tmax} distinct RM blocks of each selected row of v (rows = ciphertexts
-    i0..i0+len(v)) with uniform random bits (R#17). n2 is a multiple of 64, so a block is whole words.
-    Returns the per-row block count t (0 where row_mask is False)."""
-    rows = v.shape[0]
+def block_patches(i0: int, rows: int, seed: int, sh: Shape, tmin: int, tmax: int, row_mask=None, nthreads=None):
+    """The draws of randomise_blocks without applying them: per row t ~ U{tmin..tmax} (0 where row_mask
+    is False) and a list of (row indices, block indices, bits[len, n2/64] uint64), one entry per slot."""
     assert sh.n2 % 64 == 0
     bw = sh.n2 // 64
     t, idx = blocks(seed, TAG_ADV_BLOCKS, i0, rows, sh.n1, tmin, tmax, nthreads)
@@ -146,18 +143,28 @@ def randomise_blocks(v: np.ndarray, i0: int, seed: int, sh: Shape, tmin: int, tm
         row_mask = np.ones(rows, dtype=bool)
     t = np.where(row_mask, t, 0).astype(np.uint8)
     sel = np.nonzero(row_mask)[0]
-    if sel.size == 0:
-        return t
-    # random words for (row, slot): stream index = global row * 256 + slot
-    for slot in range(tmax):
+    patches = []
+    for slot in range(tmax if sel.size else 0):
         rr = sel[t[sel] > slot]
         if rr.size == 0:
             continue
+        # random words for (row, slot): stream index = global row * 256 + slot
         sidx = np.ascontiguousarray((i0 + rr.astype(np.uint64)) * np.uint64(256) + np.uint64(slot))
         bits = np.empty((rr.size, bw), dtype=np.uint64)
         _L().hqcgen_dense_idx(seed, TAG_ADV_BITS, sidx.ctypes.data, rr.size, sh.n2, bw, bits.ctypes.data,
                               _nt(nthreads))
-        b = idx[rr, slot].astype(np.int64)
+        patches.append((rr, idx[rr, slot].astype(np.int64), bits))
+    return t, patches
+
+
+def randomise_blocks(v: np.ndarray, i0: int, seed: int, sh: Shape, tmin: int, tmax: int, row_mask=None,
+                     nthreads=None):
+    """Overwrite t ~ U{tmin..tmax} distinct RM blocks of each selected row of v (rows = ciphertexts
+    i0..i0+len(v)) with uniform random bits (R#17). n2 is a multiple of 64, so a block is whole words.
+    Returns the per-row block count t (0 where row_mask is False)."""
+    bw = sh.n2 // 64
+    t, patches = block_patches(i0, v.shape[0], seed, sh, tmin, tmax, row_mask, nthreads)
+    for rr, b, bits in patches:
         cols = b[:, None] * bw + np.arange(bw)[None, :]
         v[rr[:, None], cols] = bits
     return t
