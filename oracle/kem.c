@@ -95,10 +95,13 @@ int orc_kem_decaps(const orc_params *p, const uint64_t *h, const uint64_t *s, co
   uint64_t *u2 = (uint64_t *)malloc(sizeof(uint64_t) * p->words);
   uint64_t *v2 = (uint64_t *)malloc(sizeof(uint64_t) * p->vwords);
   orc_encrypt(p, h, s, m, r, r + p->wr, r + 2 * p->wr, u2, v2);
-  /* compare c' with c as serialised (u bits < n, v bits < n1 n2) */
+  /* compare c' with c byte-wise over the full serialised length: the ceil(n/8) u bytes (u' has
+     zero bits in [n, 8 ceil(n/8)), so a received u with any of those bits set differs) and the n1 n2 / 8
+     v bytes; the row's words beyond the u bytes are not part of c */
   uint64_t *um = (uint64_t *)malloc(sizeof(uint64_t) * p->words);
   memcpy(um, u, sizeof(uint64_t) * p->words);
-  if (p->n % 64) um[p->words - 1] &= (~0ull) >> (64 - p->n % 64);
+  const uint32_t ubits = 8 * (uint32_t)nbytes(p->n);
+  if (ubits % 64) um[p->words - 1] &= (~0ull) >> (64 - ubits % 64);
   int eq = memcmp(um, u2, sizeof(uint64_t) * p->words) == 0 && memcmp(v, v2, sizeof(uint64_t) * p->vwords) == 0;
   kdf(p, eq ? m : sigma, u, v, K);
   free(m); free(r); free(u2); free(v2); free(um);

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
     if constexpr (CMP) {
       const uint32_t *uc = reinterpret_cast<const uint32_t *>(u_cmp + ct * P::U_STRIDE);
       for (uint32_t q = lane; q < 2 * P::U_WORDS; q += 32) {
-        const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & ((1u << P::C) - 1u) : 0u);
+        const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & P::CB_MASK : 0u);
         diff |= x ^ E[q];
       }
     } else {
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       if constexpr (CMP) {
         const uint32_t *uc = reinterpret_cast<const uint32_t *>(u_cmp + ct * P::U_STRIDE);
         for (uint32_t q = lane; q < 2 * P::U_WORDS; q += 32) {
-          const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & ((1u << P::C) - 1u) : 0u);
+          const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & P::CB_MASK : 0u);
           diff |= x ^ out[q];
         }
       } else {

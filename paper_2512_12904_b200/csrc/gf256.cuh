@@ -32,7 +32,10 @@ constexpr GfTables make_gf_tables() {
   return t;
 }
 
-__device__ __constant__ GfTables c_gf = make_gf_tables();
+// in global memory, not the constant bank: every thread of the copy below reads a different word, which
+// the constant cache would serialise (a ~3.7k-cycle prologue per CTA; profiles/r02/sb_phases.log)
+__device__ __align__(16) const GfTables g_gf = make_gf_tables();
+static_assert(sizeof(GfTables) % 16 == 0, "copied in 16-byte pieces");
 
 // compile-time GF(2^8) arithmetic for building the constant tables below and in encrypt.cuh
 constexpr uint32_t gf_mul_c(uint32_t a, uint32_t b) {  // carry-less product mod 0x11D
@@ -51,9 +54,9 @@ constexpr uint32_t gf_exp_c(uint32_t e) {  // alpha^e, alpha = 0x02
 
 // Copy the tables into a CTA's shared memory (all threads of the CTA participate).
 __device__ __forceinline__ void gf_tables_to_smem(GfTables *dst) {
-  const uint32_t *src = reinterpret_cast<const uint32_t *>(&c_gf);
-  uint32_t *d = reinterpret_cast<uint32_t *>(dst);
-  for (uint32_t i = threadIdx.x; i < sizeof(GfTables) / 4; i += blockDim.x) d[i] = src[i];
+  const uint4 *src = reinterpret_cast<const uint4 *>(&g_gf);
+  uint4 *d = reinterpret_cast<uint4 *>(dst);
+  for (uint32_t i = threadIdx.x; i < sizeof(GfTables) / 16; i += blockDim.x) d[i] = __ldg(src + i);
 }
 
 }  // namespace hqc

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "../../include/hqc_gpu.h"
 #include "launchers.h"
@@ -68,7 +69,7 @@ __global__ void k_unpack_ct(const uint8_t *__restrict__ ct, size_t ct_bytes, uin
     row(0, ub, u_words32, u_out + c * u_words32);
     row(ub, vb, v_words32, v_out + c * v_words32);
     uint32_t k = key ? key[c] : 0u;
-    k = k < nkeys ? k : nkeys - 1;  // precondition key < nkeys; clamped for memory safety
+    k = k < nkeys ? k : nkeys - 1;  // checked on the host before the launch; clamped for memory safety only
     for (uint32_t q = lane; q < y_stride; q += 32) y_out[c * y_stride + q] = y_keys[(size_t)k * y_stride + q];
   }
 }
@@ -122,7 +123,10 @@ static bool misaligned(const void *q) { return (reinterpret_cast<uintptr_t>(q) &
     if (misaligned(q)) return HQC_ERR_ALIGN; \
   } while (0)
 
+// Clear a launch error left pending by earlier, unrelated work, so that the cudaGetLastError after this
+// call's launches reports this call only (a sticky error, i.e. a dead context, persists and is reported).
 #define HQC_DISPATCH(p, fn, ...)                                 \
+  (void)cudaGetLastError();                                      \
   switch ((p)->level) {                                          \
     case 1: return fn##_l1(__VA_ARGS__);                         \
     case 3: return fn##_l3(__VA_ARGS__);                         \
@@ -192,7 +196,8 @@ extern "C" int hqc_count_mismatch(const hqc_params *p, const uint8_t *a, const u
   int s = check_level(p);
   if (s) return s;
   if (batch == 0) return HQC_OK;
-  if (!a || !b || !count) return HQC_ERR_NULL;
+  HQC_CHECK_PTR(a); HQC_CHECK_PTR(b); HQC_CHECK_PTR(count);
+  (void)cudaGetLastError();
   size_t grid = (batch + 255) / 256;
   if (grid > 4096) grid = 4096;
   k_count_mismatch<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a, b, p->k, batch, count);
@@ -204,7 +209,8 @@ extern "C" int hqc_validate_support(const hqc_params *p, const uint32_t *y, size
   int s = check_level(p);
   if (s) return s;
   if (batch == 0) return HQC_OK;
-  if (!y || !bad) return HQC_ERR_NULL;
+  HQC_CHECK_PTR(y); HQC_CHECK_PTR(bad);
+  (void)cudaGetLastError();
   size_t grid = (batch + 255) / 256;
   if (grid > 4096) grid = 4096;
   k_validate_support<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(y, p->n, p->w, p->y_stride, batch, bad);
@@ -216,6 +222,18 @@ extern "C" int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *
   if (s) return s;
   if (!grid || !wpc) return HQC_ERR_NULL;
   HQC_DISPATCH(p, shape, batch, grid, wpc);
+}
+
+extern "C" int hqc_decrypt_launch_kernel(const hqc_params *p, size_t batch) {
+  int s = check_level(p);
+  if (s) return s;
+  HQC_DISPATCH(p, kind, batch);
+}
+
+extern "C" long long hqc_decrypt_launch_count(const hqc_params *p, size_t batch) {
+  int s = check_level(p);
+  if (s) return s;
+  HQC_DISPATCH(p, nlaunch, batch);
 }
 
 extern "C" int hqc_keygen_batch(const hqc_params *p, const uint64_t *h, const uint32_t *x, const uint32_t *y,
@@ -305,6 +323,35 @@ extern "C" int hqc_kem_decaps_batch(const hqc_params *p, const uint64_t *h, cons
                (cudaStream_t)stream);
 }
 
+// ---- the host-buffer entry points' internal streams and events, created once per device (on first use)
+// and kept for the process: a per-call create/destroy costs driver calls on every request.
+struct HostPipe {
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  bool ready = false;
+};
+static std::mutex g_pipe_mu;
+static HostPipe g_pipe[16];
+
+// The device's pipe, or null if it cannot be created. The two streams are used by one call at a time:
+// g_pipe_mu is held for the whole enqueue of a call (the enqueue is asynchronous and short).
+static HostPipe *host_pipe(int *dev_out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  HostPipe &hp = g_pipe[dev];
+  if (!hp.ready) {
+    if (cudaStreamCreateWithFlags(&hp.st[0], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&hp.st[1], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hp.done[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hp.done[1], cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+    hp.ready = true;
+  }
+  *dev_out = dev;
+  return &hp;
+}
+
 // ---- host-buffer entry point: chunked, double-buffered H2D / decrypt / D2H on two internal streams
 static size_t host_row_in(const hqc_params *p) {
   return (size_t)p->u_stride * 8 + (size_t)p->v_words * 8 + (size_t)p->y_stride * 4;
@@ -341,17 +388,16 @@ extern "C" int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, 
     buf[b][2] = buf[b][1] + r16(vb) * chunk;
     buf[b][3] = buf[b][2] + r16(yb) * chunk;
   }
-  cudaStream_t caller = (cudaStream_t)stream, st[2] = {nullptr, nullptr};
-  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  cudaStream_t caller = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  int dev = 0;
+  HostPipe *hp = host_pipe(&dev);
+  if (!hp) return HQC_ERR_CUDA;
+  (void)cudaGetLastError();
+  cudaStream_t *st = hp->st;
+  cudaEvent_t start = hp->start, *done = hp->done;
   int rc = HQC_OK;
-  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess) {
-    rc = HQC_ERR_CUDA;
-  }
-  if (rc == HQC_OK) {
+  {
     cudaEventRecord(start, caller);
     cudaStreamWaitEvent(st[0], start, 0);
     cudaStreamWaitEvent(st[1], start, 0);
@@ -381,11 +427,6 @@ extern "C" int hqc_decrypt_batch_host(const hqc_params *p, const uint64_t *u_h, 
     cudaStreamWaitEvent(caller, done[0], 0);
     cudaStreamWaitEvent(caller, done[1], 0);
   }
-  for (int b = 0; b < 2; b++) {
-    if (st[b]) cudaStreamDestroy(st[b]);  // deferred until its work completes
-    if (done[b]) cudaEventDestroy(done[b]);
-  }
-  if (start) cudaEventDestroy(start);
   return rc;
 }
 
@@ -430,19 +471,20 @@ extern "C" int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_
       buf[b][i] = q;
       q += sz[i];
     }
+  if (key_h)  // key indices are host data here: checked before anything is enqueued
+    for (size_t i = 0; i < batch; i++)
+      if (key_h[i] >= nkeys) return HQC_ERR_SIZE;
+  cudaStream_t caller = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
   int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
+  HostPipe *hp = host_pipe(&dev);
+  if (!hp) return HQC_ERR_CUDA;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaStream_t caller = (cudaStream_t)stream, st[2] = {nullptr, nullptr};
-  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  (void)cudaGetLastError();
+  cudaStream_t *st = hp->st;
+  cudaEvent_t start = hp->start, *done = hp->done;
   int rc = HQC_OK;
-  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) != cudaSuccess)
-    rc = HQC_ERR_CUDA;
-  if (rc == HQC_OK) {
+  {
     cudaEventRecord(start, caller);
     cudaStreamWaitEvent(st[0], start, 0);
     cudaStreamWaitEvent(st[1], start, 0);
@@ -481,10 +523,5 @@ extern "C" int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_
     cudaStreamWaitEvent(caller, done[0], 0);
     cudaStreamWaitEvent(caller, done[1], 0);
   }
-  for (int b = 0; b < 2; b++) {
-    if (st[b]) cudaStreamDestroy(st[b]);
-    if (done[b]) cudaEventDestroy(done[b]);
-  }
-  if (start) cudaEventDestroy(start);
   return rc;
 }

@@ -28,6 +28,8 @@ int syndromes_l5(const uint8_t *sym, uint8_t *syn, size_t batch, int method, cud
   return launch_syndromes<PL>(sym, syn, batch, method, st);
 }
 int shape_l5(size_t batch, int *grid, int *wpc) { return shape_impl<PL>(batch, grid, wpc); }
+int kind_l5(size_t batch) { return kind_impl<PL>(batch); }
+long long nlaunch_l5(size_t batch) { return nlaunch_impl<PL>(batch); }
 size_t kem_ws_l5(size_t batch) { return kem_ws_bytes<PL>(batch); }
 int kem_keygen_l5(const uint8_t *seeds, uint64_t *h, uint32_t *x, uint32_t *y, uint64_t *s, uint8_t *sigma,
                    uint8_t *hpk, size_t nkeys, cudaStream_t st) {

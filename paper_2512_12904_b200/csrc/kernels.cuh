@@ -11,6 +11,7 @@
 
 #include "../../include/hqc_gpu.h"
 #include "async_copy.cuh"
+#include "exp_timing.cuh"
 #include "encrypt.cuh"
 #include "gf256.cuh"
 #include "levels.cuh"
@@ -18,13 +19,11 @@
 #include "stage1_tmem.cuh"
 #include "stage2.cuh"
 #include "stage3.cuh"
+#include "stage3_warp.cuh"
 
 namespace hqc {
 
-#ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (scripts/exp_variants.py)
-__device__ unsigned long long g_phase_cycles[16];
-#define PHASE_T0() long long _t = clock64()
-#define PHASE(i) do { long long _n = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _t)); _t = _n; } while (0)
+#ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (exp_timing.cuh)
 #define HQC_CAT2(a, b) a##b
 #define HQC_CAT(a, b) HQC_CAT2(a, b)
 extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *host8) {
@@ -33,9 +32,6 @@ extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *hos
   unsigned long long z[16] = {0};
   return cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -5;
 }
-#else
-#define PHASE_T0()
-#define PHASE(i)
 #endif
 
 
@@ -109,13 +105,16 @@ template <class P> struct S1Pipe {
   // overwrite); requests next's u, y.
   __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane, uint32_t *rout = nullptr) {
     if (rout == nullptr) rout = E;
+    PHASE_T0();
     wait();
+    PHASE(1);
     using S = DecShape<P>;    // E and the staged rows
     using ST = DecShapeT<P>;  // the lanes' product; words [ST::NOUT, NW) by s1_tail_words
     constexpr uint32_t TW = dec_tail_words<P>();
     s1_stage_d<P, S>(stg_y, dsm, lane);
     s1_build_E<P, S>(stg_u, E, lane);
     __syncwarp();
+    PHASE(2);
     if (v) issue_v(ct, lane);
     else if (has_next) issue_uy(next, lane);  // no v to stage: the next rows land during this product
     uint32_t acc[ST::R];
@@ -128,6 +127,7 @@ template <class P> struct S1Pipe {
       for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
     }
     __syncwarp();  // every lane is done reading E: r overwrites it
+    PHASE(3);
     if (v) {
       wait();  // v has landed in the staging buffer during the product loop
       s1_store_r_xor<ST>(acc, rout, stg_u, lane);
@@ -137,6 +137,7 @@ template <class P> struct S1Pipe {
       if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine;
     }
     __syncwarp();
+    PHASE(4);
     if (v && has_next) issue_uy(next, lane);
   }
 };
@@ -365,6 +366,64 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
     rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
                       act ? m_out + (base + lane) * P::K : nullptr);
     __syncwarp();
+  }
+}
+
+
+// K4s: fused decrypt for SMALL batches (BASELINE configs[0]: HQC-1 at 1,024). K4a gives every warp at
+// least 16 consecutive ciphertexts, so a batch of 1,024 occupies 64 warps on 64 SMs and the launch is the
+// latency of 16 products in a row plus a lane-per-word RS decode. Here every warp takes ONE ciphertext at a
+// time through all three stages: stage 1 by S1Pipe as in K4a, stage 2 lane per RM block, stage 3 by the
+// whole warp (stage3_warp.cuh: syndromes, Chien, Omega and Forney lane-parallel, BM over the lanes as
+// coefficients; no constant-bank tables, no CTA barrier). A CTA packs G such warps to share one copy of the
+// GF tables; the host picks G so that the batch spreads over all SMs (G = ceil(batch / SMs), capped by
+// shared memory), and warps stride over the batch when it is larger than the grid. Constant-flow.
+template <class P> struct SbSmem {
+  static constexpr uint32_t MAX_G = 16;  // warps per CTA; 512 threads: <= 128 registers
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1, 16);  // the warp's received symbols
+  static_assert(RsWarpScratch<P>::BYTES <= WarpSmem<P>::E_BYTES, "the RS scratch reuses the warp's E");
+  static constexpr uint32_t WARP_BYTES = WarpSmem<P>::S1_BYTES + SYM_BYTES;
+  static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + g * WARP_BYTES; }
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out,
+                                                                        size_t batch) {
+  using M = SbSmem<P>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + (size_t)wib * M::WARP_BYTES;
+  uint8_t *sym = ws + WarpSmem<P>::S1_BYTES;
+  PHASE_T0();
+  S1Pipe<P> pipe(ws, u, v, y, lane);
+  const size_t step = (size_t)gridDim.x * (blockDim.x >> 5);
+  size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (ct < batch) pipe.issue_uy(ct, lane);  // the first rows are in flight while the GF tables are copied
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  PHASE(0);
+  for (; ct < batch; ct += step) {
+    pipe.run(ct, ct + step < batch, ct + step, lane);
+    PHASE_T0();
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in E)
+      const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      sym[j] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+    __syncwarp();  // the symbols are complete and r (in E) is consumed
+    PHASE(5);
+    rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(pipe.E), lane, m_out + ct * P::K);
+    __syncwarp();  // E and sym are free for the next ciphertext
+    PHASE(7);
   }
 }
 
@@ -812,15 +871,43 @@ template <class P> static uint32_t decrypt_ws_smem() { return GF_BYTES + WsSmem<
 template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_BYTES; }
 
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
-// 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t). HQC_DEC_KERNEL=1..4 overrides
-// (experiments and tests).
-template <class P> static int dec_kernel() {
+// 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s).
+// HQC_DEC_KERNEL=1..5 overrides (experiments and tests).
+static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  if (env >= 1 && env <= 4) return env;
+  return env >= 1 && env <= 5 ? env : 0;
+}
+template <class P> static int dec_kernel() {
+  if (dec_kernel_env()) return dec_kernel_env();
   return P::level == 3 ? 2 : 1;  // occupancy sweeps: one warp wins for HQC-1 (0.629 vs 0.645 ms) and HQC-5
+}
+// Read on every call (experiments sweep them within one process): HQC_SB_MAX = the largest batch that
+// takes K4s by default; HQC_DEC_SPLIT = the most ciphertexts one launch of the large-batch kernels takes.
+static long env_long(const char *name, long dflt) {
+  const char *s = getenv(name);
+  return s && *s ? atol(s) : dflt;
+}
+// K4s up to this batch (scripts/sweep_launch.py small / large, profiles/r02/sweep_*.log):
+// HQC-3 at every batch (65,536: 5.61e7/s vs 5.41e7 for the warp pair K4; 262,144: 5.79e7 vs 5.53e7);
+// HQC-1 up to 32,768 (1.02e8 vs 9.18e7; at 65,536 K4a's paired RM stage and lane-per-word RS win,
+// 1.19e8 vs 1.05e8); HQC-5 up to 8,192 (its shared memory allows 10 warps per SM in K4s, 16 in K4a).
+template <class P> static size_t sb_max_batch(int sms) {
+  const long dflt = P::level == 3 ? -1L : (long)sms * (P::level == 1 ? 224 : 56);
+  const long v = env_long("HQC_SB_MAX", dflt);
+  return v < 0 ? ~(size_t)0 : (size_t)v;
+}
+template <class P> static int dec_kernel_for(int sms, size_t batch) {
+  if (dec_kernel_env()) return dec_kernel_env();
+  return batch <= sb_max_batch<P>(sms) ? 5 : dec_kernel<P>();
+}
+// The largest group (warps per CTA) of K4s whose shared memory fits one CTA.
+template <class P> constexpr uint32_t sb_max_g() {
+  uint32_t g = SbSmem<P>::MAX_G;
+  while (g > 1 && SbSmem<P>::bytes(g) > 227u * 1024u) g--;
+  return g;
 }
 template <class P> static bool use_pair() { return dec_kernel<P>() == 2; }
 // Which standalone product kernel: 1 = one warp per ciphertext (k_stage1), 2 = warp pair with the output
@@ -858,6 +945,8 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaFuncSetAttribute(k_decrypt_ws<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_ws<P>, 128, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt_ws[P::level] = c > 0 ? c : 1;
+  if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SbSmem<P>::bytes(sb_max_g<P>()))) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   di.ready[P::level] = true;
@@ -875,7 +964,18 @@ static int cur_device(DevInfo **out) {
 // least MIN_PER ciphertexts (the lane-per-ciphertext RS stage wants full chunks).
 constexpr size_t MIN_PER = 32;
 template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *grid, size_t *per) {
-  const int kind = dec_kernel<P>();
+  const int kind = dec_kernel_for<P>(di.sms, batch);
+  if (kind == 5) {  // groups of G ciphertexts (G warps per CTA) spread over all SMs; *per = G
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > sb_max_g<P>()) g = sb_max_g<P>();
+    *per = g;
+    size_t groups = (batch + g - 1) / g;
+    const size_t cap = (size_t)di.sms * (227u * 1024u / SbSmem<P>::bytes((uint32_t)g) > 0
+                                             ? 227u * 1024u / SbSmem<P>::bytes((uint32_t)g) : 1u);
+    *grid = (int)(groups < cap ? groups : cap);
+    return;
+  }
   if (kind == 4) {  // one CTA of WARPS warps per SM; at least 16 ciphertexts per warp
     const size_t warps = (size_t)di.sms * TmDec<P>::WARPS;
     size_t pw = (batch + warps - 1) / warps;
@@ -899,16 +999,23 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
   *grid = (int)((batch + *per - 1) / *per);
 }
 
+// Largest batch of one launch of the persistent kernels (0 = unlimited): a long contiguous range per CTA
+// lets the CTAs drift out of lockstep, so a big batch runs as consecutive launches.
+template <class P> static size_t dec_split() {
+  const long s = env_long("HQC_DEC_SPLIT", -1);
+  if (s >= 0) return (size_t)s;
+  // measured at 4,194,304 (scripts/sweep_launch.py split, profiles/r02/sweep_split.log): HQC-1 +7% at 65,536
+  // per launch, HQC-5 +9% at 262,144; the HQC-3 warp pair is fastest unsplit
+  return P::level == 1 ? 65536u : P::level == 5 ? 262144u : 0u;
+}
+
 template <class P>
-static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *y, uint8_t *m, size_t batch,
-                          cudaStream_t st) {
-  DevInfo *di;
-  const int dev = cur_device(&di);
-  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v, const uint32_t *y, uint8_t *m,
+                              size_t batch, cudaStream_t st) {
   int grid;
   size_t per;
   decrypt_shape<P>(*di, batch, &grid, &per);
-  switch (dec_kernel<P>()) {
+  switch (dec_kernel_for<P>(di->sms, batch)) {
     case 1: k_decrypt_w1<P><<<grid, 32, decrypt_w1_smem<P>(), st>>>(u, v, y, m, batch, per); break;
     case 2: k_decrypt<P><<<grid, DEC_THREADS, decrypt_smem<P>(), st>>>(u, v, y, m, batch, per); break;
     case 4:
@@ -917,9 +1024,29 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
         return HQC_ERR_CUDA;
       k_decrypt_t<P><<<grid, 32 * TmDec<P>::WARPS, decrypt_t_smem<P>(), st>>>(u, v, y, m, batch, per);
       break;
+    case 5:
+      k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      break;
     default: k_decrypt_ws<P><<<grid, 128, decrypt_ws_smem<P>(), st>>>(u, v, y, m, batch, per); break;
   }
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+}
+
+template <class P>
+static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *y, uint8_t *m, size_t batch,
+                          cudaStream_t st) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  const size_t split = dec_split<P>();
+  if (split == 0 || batch <= split) return launch_decrypt_one<P>(di, u, v, y, m, batch, st);
+  for (size_t off = 0; off < batch; off += split) {
+    const size_t n = batch - off < split ? batch - off : split;
+    const int rc = launch_decrypt_one<P>(di, u + off * P::U_STRIDE, v + off * P::V_WORDS, y + off * P::Y_STRIDE,
+                                         m + off * P::K, n, st);
+    if (rc != HQC_OK) return rc;
+  }
+  return HQC_OK;
 }
 
 template <class P>
@@ -989,14 +1116,8 @@ static int launch_keygen(const uint64_t *h, const uint32_t *x, const uint32_t *y
 }
 
 // Which encrypt kernel: 2 = warp pair with per-key cached E (k_encrypt2, default), 1 = one warp per
-// ciphertext (k_encrypt). HQC_ENC_KERNEL overrides (tests, experiments).
-static int enc_kernel() {
-  static int env = [] {
-    const char *s = getenv("HQC_ENC_KERNEL");
-    return s ? atoi(s) : 0;
-  }();
-  return env == 1 ? 1 : 2;
-}
+// ciphertext (k_encrypt). HQC_ENC_KERNEL overrides (tests, experiments; read on every call).
+static int enc_kernel() { return env_long("HQC_ENC_KERNEL", 2) == 1 ? 1 : 2; }
 
 // Launch the encrypt kernel (CMP: the KEM re-encryption check writing two flags per ciphertext to eq2).
 template <class P, bool CMP>
@@ -1039,13 +1160,28 @@ static int launch_encrypt(const uint64_t *h, const uint64_t *s, const uint32_t *
   return launch_encrypt_any<P, false>(h, s, key, m, r1, r2, e, u, v, batch, nullptr, nullptr, nullptr, st);
 }
 
+// Which fused kernel hqc_decrypt_batch launches for `batch` on the current device (1..5 as dec_kernel).
+template <class P> static int kind_impl(size_t batch) {
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
+  return dec_kernel_for<P>(di->sms, batch);
+}
+
+// How many kernel launches hqc_decrypt_batch makes for `batch` (the large-batch split, dec_split).
+template <class P> static long long nlaunch_impl(size_t batch) {
+  const size_t split = dec_split<P>();
+  return batch == 0 ? 0 : (split == 0 || batch <= split) ? 1 : (long long)((batch + split - 1) / split);
+}
+
 template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
-  *wpc = dec_kernel<P>() == 1 ? 1 : dec_kernel<P>() == 2 ? DEC_THREADS / 32 : dec_kernel<P>() == 4 ? TmDec<P>::WARPS : 4;
+  const int kind = dec_kernel_for<P>(di->sms, batch);
+  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : kind == 5 ? (int)per : 4;
   return HQC_OK;
 }
 

@@ -18,6 +18,8 @@
                    const uint32_t *r1, const uint32_t *r2, const uint32_t *e, uint64_t *u, uint64_t *v,        \
                    size_t batch, cudaStream_t st);                                                              \
   int shape_l##L(size_t batch, int *grid, int *wpc);                                                            \
+  int kind_l##L(size_t batch);                                                                                  \
+  long long nlaunch_l##L(size_t batch);                                                                         \
   int syndromes_l##L(const uint8_t *sym, uint8_t *syn, size_t batch, int method, cudaStream_t st);              \
   size_t kem_ws_l##L(size_t batch);                                                                             \
   int kem_keygen_l##L(const uint8_t *seeds, uint64_t *h, uint32_t *x, uint32_t *y, uint64_t *s, uint8_t *sigma,    \

@@ -30,6 +30,9 @@ template <int LEVEL> struct Lv : Table1<LEVEL> {
   static constexpr uint32_t Q0 = N / 32;               // word holding bit n-1
   static constexpr uint32_t C = N % 32;                // bits of u in word Q0 (nonzero: n is prime)
   static_assert(C != 0, "n must not be a multiple of 32");
+  // bits of word Q0 inside the ceil(n/8) serialized u bytes: the KEM's byte-wise compare
+  static constexpr uint32_t CB = round_up(C, 8);
+  static constexpr uint32_t CB_MASK = CB >= 32 ? 0xFFFFFFFFu : (1u << CB) - 1u;
   static_assert(N12 % 128 == 0, "r is processed in 16-byte chunks");
   static_assert(N2 % 128 == 0 && (N2 / 32) % 4 == 0, "RM blocks are whole 16-byte chunks");
   static_assert(N1 - K == TWO_DELTA, "shortened RS: n1 - k = 2 delta");

@@ -51,6 +51,7 @@ __device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) 
   constexpr uint32_t NV = P::Q0 / 4;
   constexpr uint32_t MASK_C = (1u << P::C) - 1u;
   static_assert(P::Q0 + 1 < 2 * P::U_STRIDE, "the staged row has a padding word after word Q0");
+  static_assert(S::E_WORDS >= 2 * P::Q0 + 2, "E holds the doubled u: every path below writes E[2 Q0 + 1]");
   const uint32_t eq0 = su[P::Q0] & MASK_C;
   for (uint32_t c = lane; c < NV; c += NT)
     reinterpret_cast<uint4 *>(E)[c] = reinterpret_cast<const uint4 *>(su)[c];

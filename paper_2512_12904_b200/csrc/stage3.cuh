@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "gf256.cuh"
+#include "exp_timing.cuh"
 #include "levels.cuh"
 
 namespace hqc {
@@ -104,6 +105,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   uint16_t *lOdd = lS + TD * 32;
   uint16_t *sLam = lOdd;  // read completely before lOdd is written
   using LIN = RsLinear<P>;
+  PHASE_T0();
 
   // ---- syndromes S_i = sum_j sym_j alpha^{ij} (i = 1..2delta) as the GF(2)-linear map SYN
   {
@@ -123,6 +125,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
 #pragma unroll
     for (int i = 0; i < TD; i++) lS[i * 32 + lane] = LOGT[(Sw[i / 4] >> (8 * (i % 4))) & 0xFFu];
   }
+  PHASE(9);
 
   // ---- Berlekamp–Massey (Massey 1969) with Bx = x^m * B, logs of Bx kept
   uint32_t Lam[DL + 1], lBx[DL + 1], lLam[DL + 1];
@@ -152,6 +155,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     L = grow ? (uint32_t)r + 1 - L : L;
     lb = grow ? ld : lb;
   }
+  PHASE(10);
   uint32_t deg = 0;
 #pragma unroll
   for (int k = 0; k <= DL; k++) {
@@ -213,6 +217,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     }
   }
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
+  PHASE(11);
 
   // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta, from i = 2delta-1 down:
   //      Omega_i reads log S_{i'+1} for i' <= i only, so it may overwrite row i in place
@@ -225,6 +230,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     lOm[i * 32 + lane] = LOGT[om];
   }
 
+  PHASE(12);
   // ---- Forney on the message positions, then the output bytes. Omega(alpha^-j) = sum_i Omega_i alpha^{-ij}
   //      for all k message positions at once: each log Omega_i is read once, and the exponents -ij mod 255
   //      are compile-time constants (immediate offsets into EXPT; no modular arithmetic at run time).
@@ -251,6 +257,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     const uint32_t fix = (ok && ((rootmask >> j) & 1u)) ? ej : 0u;
     outw[j / 4] |= ((sym_at(j) ^ fix) & 0xFFu) << (8 * (j % 4));
   }
+  PHASE(13);
   if (out != nullptr) {
     if constexpr (K % 16 == 0) {
 #pragma unroll

@@ -1,0 +1,147 @@
+// Stage 3 — shortened RS decoding of ONE received word by a whole warp. Same algorithm
+// and the same decisions as the lane-per-word decoder of stage3.cuh (readings R#4-R#7: syndromes
+// S_i = r(alpha^i), i = 1..2delta; Berlekamp–Massey with Lambda and x^m B truncated to delta+1
+// coefficients; Chien search over j < n1; ok = L <= delta and deg Lambda = L and #roots = L; Forney with
+// b = 1 on the k message positions; output sym[0..k) corrected iff ok), with the work spread over the
+// lanes instead of over 32 words:
+//   syndromes   lane i (and i + 32) accumulates S_{i+1} = XOR_j EXP[log sym_j + (i+1) j mod 255]
+//   BM          lane t holds coefficient t of Lambda and of x^m B (t <= delta < 32); the discrepancy is a
+//               warp XOR-reduction (REDUX), the shift by x a shuffle; L, log b, d are warp-uniform
+//   Chien       lane j (and j + 32, j + 64) evaluates Lambda(alpha^-j) and its odd part
+//   Omega       lane i (and i + 32) forms Omega_i = sum_t Lambda_t S_{i-t+1}
+//   Forney      lane j < k corrects message byte j
+// It exists for SMALL batches (k_decrypt_sb): a lane-per-word decoder runs ~15k dependent instructions on
+// one lane and reads its GF(2)-linear tables from the constant bank, cold in a short launch (profiles/r02/
+// sb_phases.log: 90k cycles for HQC-1); this one is a few hundred instructions per lane on the log/antilog
+// tables in shared memory. Every loop count is fixed by the level; the data selects, never branches.
+#pragma once
+#include <cstdint>
+
+#include "gf256.cuh"
+#include "levels.cuh"
+#include "stage3.cuh"
+
+namespace hqc {
+
+// Per-warp scratch (uint16 logs): log sym_j (n1), a sentinel pad of delta+1 rows then log S_{i+1} (2delta),
+// log Lambda_t (delta+1), log Omega_i (2delta).
+template <class P> struct RsWarpScratch {
+  static constexpr uint32_t PAD = P::DELTA + 1;
+  static constexpr uint32_t LSYM = 0, LS = P::N1 + PAD, LLAM = LS + P::TWO_DELTA, LOM = LLAM + P::DELTA + 1;
+  static constexpr uint32_t HALFS = LOM + P::TWO_DELTA;
+  static constexpr uint32_t BYTES = round_up(HALFS * 2, 16);
+  static_assert(P::DELTA < 32 && P::K <= 32, "one lane per Lambda coefficient and per message byte");
+};
+
+// sym: the word's n1 received symbols (shared memory); scr: RsWarpScratch<P>::BYTES of shared memory;
+// out: k message bytes (global), or null. Returns ok (warp-uniform).
+template <class P>
+__device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfTables *gf, uint16_t *scr, int lane,
+                                                   uint8_t *out) {
+  using W = RsWarpScratch<P>;
+  constexpr int TD = P::TWO_DELTA, DL = P::DELTA, N1 = P::N1, K = P::K;
+  constexpr int NI = (TD + 31) / 32, NJ = (N1 + 31) / 32;  // rounds of the lane-parallel loops
+  const uint8_t *EXPT = gf->exp;
+  const uint16_t *LOGT = gf->log;
+  uint16_t *lsym = scr + W::LSYM, *lS = scr + W::LS, *lLam = scr + W::LLAM, *lOm = scr + W::LOM;
+  for (int j = lane; j < N1; j += 32) lsym[j] = LOGT[sym[j]];
+  for (int t = lane; t < (int)W::PAD; t += 32) lS[t - (int)W::PAD] = GF_LOG0;  // log S_i for i <= 0
+  __syncwarp();
+
+  // ---- syndromes: S_{i+1} = sum_j sym_j alpha^{(i+1) j}; the exponent advances by i+1 per symbol
+  {
+    uint32_t s[NI], e[NI];
+#pragma unroll
+    for (int q = 0; q < NI; q++) s[q] = 0, e[q] = 0;
+#pragma unroll 2
+    for (int j = 0; j < N1; j++) {
+      const uint32_t ls = lsym[j];
+#pragma unroll
+      for (int q = 0; q < NI; q++) {
+        s[q] ^= EXPT[ls + e[q]];
+        const uint32_t i1 = (uint32_t)(lane + 32 * q + 1) % 255u;
+        e[q] = mod255_add(e[q], i1);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NI; q++)
+      if (lane + 32 * q < TD) lS[lane + 32 * q] = LOGT[s[q]];
+  }
+  __syncwarp();
+
+  // ---- Berlekamp–Massey: lane t <= delta holds Lambda_t and log (x^m B)_t
+  const bool coef = lane <= DL;
+  uint32_t lam = lane == 0 ? 1u : 0u;
+  uint32_t lbx = lane == 1 ? 0u : GF_LOG0;  // Bx = x * 1
+  uint32_t L = 0, lb = 0;
+#pragma unroll 1
+  for (int r = 0; r < TD; r++) {
+    const uint32_t llam = LOGT[lam];
+    const uint32_t term = coef ? EXPT[llam + lS[r - lane]] : 0u;  // Lambda_t S_{r+1-t} (sentinel for r < t)
+    const uint32_t d = __reduce_xor_sync(0xffffffffu, term);
+    const uint32_t ld = LOGT[d];
+    const uint32_t lc = d ? mod255_sub(ld, lb) : GF_LOG0;  // log(d / b)
+    const bool grow = (d != 0) && (2 * L <= (uint32_t)r);
+    lam ^= coef ? EXPT[lc + lbx] : 0u;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, grow ? llam : lbx, 1);
+    lbx = (lane == 0 || !coef) ? GF_LOG0 : up;
+    L = grow ? (uint32_t)r + 1 - L : L;
+    lb = grow ? ld : lb;
+  }
+  const uint32_t nzmask = __ballot_sync(0xffffffffu, coef && lam != 0);
+  const uint32_t deg = 31u - __clz(nzmask);  // Lambda_0 = 1 always
+  if (coef) lLam[lane] = LOGT[lam];
+  __syncwarp();
+
+  // ---- Chien search over j < n1 (lane j + 32 q); the odd part of Lambda(alpha^-j) kept for j < k
+  uint32_t nroots = 0, root_mine = 0, lodd_mine = GF_LOG0;
+#pragma unroll
+  for (int q = 0; q < NJ; q++) {
+    const int j = lane + 32 * q;
+    uint32_t ev = 0, od = 0, e = 0;  // e = (-j t) mod 255
+    const uint32_t jm = (uint32_t)j % 255u;
+#pragma unroll
+    for (int t = 0; t <= DL; t++) {
+      const uint32_t x = EXPT[lLam[t] + e];
+      if (t & 1) od ^= x; else ev ^= x;
+      e = mod255_sub(e, jm);
+    }
+    const bool root = (j < N1) && (ev == od);
+    nroots += __popc(__ballot_sync(0xffffffffu, root));
+    if (q == 0) {
+      root_mine = root ? 1u : 0u;
+      lodd_mine = LOGT[od];
+    }
+  }
+  const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
+
+  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta
+#pragma unroll
+  for (int q = 0; q < NI; q++) {
+    const int i = lane + 32 * q;
+    uint32_t om = 0;
+#pragma unroll
+    for (int t = 0; t <= DL; t++) om ^= EXPT[lLam[t] + lS[i - t]];
+    if (i < TD) lOm[i] = LOGT[om];
+  }
+  __syncwarp();
+
+  // ---- Forney on message position j = lane < k: e_j = Omega(alpha^-j) / (alpha^j Lambda_odd(alpha^-j))
+  if (lane < K) {
+    const uint32_t jm = (uint32_t)lane % 255u;
+    uint32_t acc = 0, e = 0;  // e = (-i j) mod 255
+#pragma unroll 4
+    for (int i = 0; i < TD; i++) {
+      acc ^= EXPT[lOm[i] + e];
+      e = mod255_sub(e, jm);
+    }
+    const uint32_t lnum = LOGT[acc];
+    const uint32_t le = mod255_sub(mod255_sub(lnum == GF_LOG0 ? 0u : lnum, jm), lodd_mine == GF_LOG0 ? 0u : lodd_mine);
+    const uint32_t ej = (lnum == GF_LOG0 || lodd_mine == GF_LOG0) ? 0u : EXPT[le];
+    const uint32_t fix = (ok && root_mine) ? ej : 0u;
+    if (out != nullptr) out[lane] = (uint8_t)(sym[lane] ^ fix);
+  }
+  return ok ? 1u : 0u;
+}
+
+}  // namespace hqc

@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
             "hqc_count_mismatch": [P, vp, vp, sz, vp, vp],
             "hqc_validate_support": [P, vp, sz, vp, vp],
             "hqc_decrypt_launch_shape": [P, sz, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+            "hqc_decrypt_launch_kernel": [P, sz],
             "hqc_keygen_batch": [P, vp, vp, vp, vp, sz, vp],
             "hqc_encrypt_batch": [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hqc_kem_hpk_batch": [P, vp, vp, vp, sz, vp],
@@ -93,6 +94,8 @@ def lib() -> ctypes.CDLL:
         L.hqc_decrypt_ct_host_workspace_bytes.restype = sz
         L.hqc_decrypt_ct_batch_host.argtypes = [P, vp, vp, vp, sz, vp, sz, vp, sz, sz, vp]
         L.hqc_decrypt_ct_batch_host.restype = i32
+        L.hqc_decrypt_launch_count.argtypes = [P, sz]
+        L.hqc_decrypt_launch_count.restype = ctypes.c_longlong
         L.hqc_status_str.argtypes = [i32]
         L.hqc_status_str.restype = ctypes.c_char_p
         _lib = L
@@ -134,6 +137,28 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _need(cond: bool, msg: str) -> None:
+    """Argument check that survives python -O (unlike assert)."""
+    if not cond:
+        raise HqcError(msg)
+
+
+def _keys_in_range(key_index, nkeys: int, batch: int, check: bool) -> None:
+    """key_index (None: row i uses key i) must address rows of the per-key tables: the kernels index them
+    without a bound (the C ABI has no key count), so an out-of-range index would read out of bounds. On a
+    CUDA tensor the check costs one reduction and a synchronisation; check=False skips it."""
+    if key_index is None:
+        _need(batch <= nkeys, f"no key_index: {batch} rows need {batch} keys, got {nkeys}")
+        return
+    _need(_rows(key_index, 4, "key_index") == batch, "key_index: one uint32 per row")
+    if check and batch:
+        import torch
+
+        k = key_index.view(torch.int32) if key_index.dtype != torch.int32 else key_index
+        lo, hi = int(k.min().item()), int(k.max().item())
+        _need(0 <= lo and hi < nkeys, f"key_index out of range [0, {nkeys}): min {lo}, max {hi}")
+
+
 def _rows(t, row_bytes: int, name: str) -> int:
     nbytes = t.numel() * t.element_size()
     if nbytes % row_bytes:
@@ -145,8 +170,8 @@ def hqc_decrypt_batch(level: int, u, v, y_support, m_out, stream=None) -> None:
     """m_out[b] = C.Decode(v[b] ^ trunc(u[b] * y[b])) — the fused kernel."""
     p = params(level)
     B = _rows(u, 8 * p.u_stride, "u")
-    assert _rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B
-    assert _rows(m_out, p.k, "m_out") == B
+    _need(_rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B, "row counts of the arguments disagree")
+    _need(_rows(m_out, p.k, "m_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_decrypt_batch(ctypes.byref(_cp(level)), _ptr(u), _ptr(v), _ptr(y_support), _ptr(m_out), B,
                                    _stream(stream)))
 
@@ -154,7 +179,7 @@ def hqc_decrypt_batch(level: int, u, v, y_support, m_out, stream=None) -> None:
 def hqc_sparse_dense_mul_batch(level: int, u, y_support, v, r_out, stream=None) -> None:
     p = params(level)
     B = _rows(u, 8 * p.u_stride, "u")
-    assert _rows(r_out, 8 * p.v_words, "r_out") == B
+    _need(_rows(r_out, 8 * p.v_words, "r_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_sparse_dense_mul_batch(ctypes.byref(_cp(level)), _ptr(u), _ptr(y_support), _ptr(v),
                                             _ptr(r_out), B, _stream(stream)))
 
@@ -162,14 +187,14 @@ def hqc_sparse_dense_mul_batch(level: int, u, y_support, v, r_out, stream=None) 
 def hqc_rm_decode_batch(level: int, r, sym_out, stream=None) -> None:
     p = params(level)
     B = _rows(r, 8 * p.v_words, "r")
-    assert _rows(sym_out, p.n1, "sym_out") == B
+    _need(_rows(sym_out, p.n1, "sym_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_rm_decode_batch(ctypes.byref(_cp(level)), _ptr(r), _ptr(sym_out), B, _stream(stream)))
 
 
 def hqc_rs_decode_batch(level: int, sym, m_out, ok_out=None, stream=None) -> None:
     p = params(level)
     B = _rows(sym, p.n1, "sym")
-    assert _rows(m_out, p.k, "m_out") == B
+    _need(_rows(m_out, p.k, "m_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_rs_decode_batch_ex(ctypes.byref(_cp(level)), _ptr(sym), _ptr(m_out), _ptr(ok_out), B,
                                         _stream(stream)))
 
@@ -181,7 +206,7 @@ def hqc_rs_syndromes_batch(level: int, sym, syn_out, method: str = "linear", str
     """S_1..S_2delta of each received word (step a6); method: linear | nibble | logexp."""
     p = params(level)
     B = _rows(sym, p.n1, "sym")
-    assert _rows(syn_out, 2 * p.delta, "syn_out") == B
+    _need(_rows(syn_out, 2 * p.delta, "syn_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_rs_syndromes_batch(ctypes.byref(_cp(level)), _ptr(sym), _ptr(syn_out), B, SYN_METHODS[method],
                                         _stream(stream)))
 
@@ -206,23 +231,47 @@ def hqc_decrypt_launch_shape(level: int, batch: int) -> tuple[int, int]:
     return g.value, w.value
 
 
+KERNEL_NAMES = {1: "k_decrypt_w1 (fused, one warp per ciphertext range, lane-per-word RS)",
+                2: "k_decrypt (fused, warp pair)", 3: "k_decrypt_ws (fused, warp-specialised)",
+                4: "k_decrypt_t (fused, tensor-memory product)",
+                5: "k_decrypt_sb (fused, one warp per ciphertext, warp-parallel RS)"}
+
+
+def hqc_decrypt_launch_kernel(level: int, batch: int) -> int:
+    """Which fused kernel hqc_decrypt_batch launches for `batch` (KERNEL_NAMES)."""
+    k = int(lib().hqc_decrypt_launch_kernel(ctypes.byref(_cp(level)), batch))
+    _check(min(k, 0))
+    return k
+
+
+def hqc_decrypt_launch_count(level: int, batch: int) -> int:
+    """How many kernel launches hqc_decrypt_batch makes for `batch`."""
+    n = int(lib().hqc_decrypt_launch_count(ctypes.byref(_cp(level)), batch))
+    _check(min(n, 0))
+    return n
+
+
 def hqc_keygen_batch(level: int, h, x, y, s_out, stream=None) -> None:
     """s = x + h*y per key (Alg. 3)."""
     p = params(level)
     K = _rows(h, 8 * p.u_stride, "h")
-    assert _rows(x, 4 * p.y_stride, "x") == K and _rows(y, 4 * p.y_stride, "y") == K
-    assert _rows(s_out, 8 * p.u_stride, "s_out") == K
+    _need(_rows(x, 4 * p.y_stride, "x") == K and _rows(y, 4 * p.y_stride, "y") == K, "row counts of the arguments disagree")
+    _need(_rows(s_out, 8 * p.u_stride, "s_out") == K, "row counts of the arguments disagree")
     _check(lib().hqc_keygen_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(x), _ptr(y), _ptr(s_out), K,
                                   _stream(stream)))
 
 
-def hqc_encrypt_batch(level: int, h, s, key_index, m, r1, r2, e, u_out, v_out, stream=None) -> None:
+def hqc_encrypt_batch(level: int, h, s, key_index, m, r1, r2, e, u_out, v_out, stream=None,
+                      check_keys: bool = True) -> None:
     """u = r1 + h*r2, v = trunc(mG + s*r2 + e) per ciphertext (Alg. 1); key_index may be None."""
     p = params(level)
     B = _rows(m, p.k, "m")
+    nk = _rows(h, 8 * p.u_stride, "h")
+    _need(_rows(s, 8 * p.u_stride, "s") == nk, "h and s: one row per key each")
+    _keys_in_range(key_index, nk, B, check_keys)
     for t, nm in ((r1, "r1"), (r2, "r2"), (e, "e")):
-        assert _rows(t, 4 * p.e_stride, nm) == B
-    assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
+        _need(_rows(t, 4 * p.e_stride, nm) == B, "row counts of the arguments disagree")
+    _need(_rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_encrypt_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(key_index), _ptr(m), _ptr(r1),
                                    _ptr(r2), _ptr(e), _ptr(u_out), _ptr(v_out), B, _stream(stream)))
 
@@ -239,7 +288,7 @@ def hqc_kem_hpk_batch(level: int, h, s, hpk_out, stream=None) -> None:
     """H_pk = SHAKE256(h bytes || s bytes || 0x02, 32) per key (R#20-R#21)."""
     p = params(level)
     K = _rows(h, 8 * p.u_stride, "h")
-    assert _rows(s, 8 * p.u_stride, "s") == K and _rows(hpk_out, 32, "hpk_out") == K
+    _need(_rows(s, 8 * p.u_stride, "s") == K and _rows(hpk_out, 32, "hpk_out") == K, "row counts of the arguments disagree")
     _check(lib().hqc_kem_hpk_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk_out), K, _stream(stream)))
 
 
@@ -247,33 +296,41 @@ def hqc_kem_keygen_batch(level: int, seeds, h_out, x_out, y_out, s_out, sigma_ou
     """KeyGen from 32-byte seeds (R#24): h, x, y, sigma by SHAKE256 expansion, s = x + h*y, H_pk."""
     p = params(level)
     K = _rows(seeds, 32, "seeds")
-    assert _rows(h_out, 8 * p.u_stride, "h_out") == K and _rows(s_out, 8 * p.u_stride, "s_out") == K
-    assert _rows(x_out, 4 * p.y_stride, "x_out") == K and _rows(y_out, 4 * p.y_stride, "y_out") == K
-    assert _rows(sigma_out, p.k, "sigma_out") == K
+    _need(_rows(h_out, 8 * p.u_stride, "h_out") == K and _rows(s_out, 8 * p.u_stride, "s_out") == K, "row counts of the arguments disagree")
+    _need(_rows(x_out, 4 * p.y_stride, "x_out") == K and _rows(y_out, 4 * p.y_stride, "y_out") == K, "row counts of the arguments disagree")
+    _need(_rows(sigma_out, p.k, "sigma_out") == K, "row counts of the arguments disagree")
     if hpk_out is not None:
-        assert _rows(hpk_out, 32, "hpk_out") == K
+        _need(_rows(hpk_out, 32, "hpk_out") == K, "row counts of the arguments disagree")
     _check(lib().hqc_kem_keygen_batch(ctypes.byref(_cp(level)), _ptr(seeds), _ptr(h_out), _ptr(x_out), _ptr(y_out),
                                       _ptr(s_out), _ptr(sigma_out), _ptr(hpk_out), K, _stream(stream)))
 
 
-def hqc_kem_encaps_batch(level: int, h, s, hpk, key_index, m, u_out, v_out, K_out, workspace, stream=None) -> None:
+def hqc_kem_encaps_batch(level: int, h, s, hpk, key_index, m, u_out, v_out, K_out, workspace, stream=None,
+                         check_keys: bool = True) -> None:
     """HHK Encaps with caller-drawn messages m: coins(H_pk, m) -> Encrypt -> K (R#20-R#23)."""
     p = params(level)
     B = _rows(m, p.k, "m")
-    assert _rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B
-    assert _rows(K_out, 64, "K_out") == B
+    nk = _rows(h, 8 * p.u_stride, "h")
+    _need(_rows(s, 8 * p.u_stride, "s") == nk and _rows(hpk, 32, "hpk") == nk, "h, s, hpk: one row per key each")
+    _keys_in_range(key_index, nk, B, check_keys)
+    _need(_rows(u_out, 8 * p.u_stride, "u_out") == B and _rows(v_out, 8 * p.v_words, "v_out") == B, "row counts of the arguments disagree")
+    _need(_rows(K_out, 64, "K_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_kem_encaps_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk), _ptr(key_index), _ptr(m),
                                       _ptr(u_out), _ptr(v_out), _ptr(K_out), B, _ptr(workspace), _nbytes(workspace),
                                       _stream(stream)))
 
 
 def hqc_kem_decaps_batch(level: int, h, s, hpk, sigma, key_index, y_support, u, v, K_out, accepted_out, workspace,
-                         stream=None) -> None:
+                         stream=None, check_keys: bool = True) -> None:
     """HHK Decaps with implicit rejection: Decrypt -> coins -> re-encrypt and compare -> K (R#20-R#23).
     h, s, hpk, sigma, y_support are per KEY; key_index (None = identity) maps rows to keys."""
     p = params(level)
     B = _rows(u, 8 * p.u_stride, "u")
-    assert _rows(v, 8 * p.v_words, "v") == B and _rows(K_out, 64, "K_out") == B
+    nk = _rows(h, 8 * p.u_stride, "h")
+    _need(_rows(s, 8 * p.u_stride, "s") == nk and _rows(hpk, 32, "hpk") == nk and _rows(sigma, p.k, "sigma") >= nk
+          and _rows(y_support, 4 * p.y_stride, "y_support") == nk, "h, s, hpk, sigma, y_support: one row per key each")
+    _keys_in_range(key_index, nk, B, check_keys)
+    _need(_rows(v, 8 * p.v_words, "v") == B and _rows(K_out, 64, "K_out") == B, "row counts of the arguments disagree")
     _check(lib().hqc_kem_decaps_batch(ctypes.byref(_cp(level)), _ptr(h), _ptr(s), _ptr(hpk), _ptr(sigma),
                                       _ptr(key_index), _ptr(y_support), _ptr(u), _ptr(v), _ptr(K_out),
                                       _ptr(accepted_out), B, _ptr(workspace), _nbytes(workspace), _stream(stream)))
@@ -297,8 +354,8 @@ def hqc_decrypt_batch_host(level: int, u, v, y_support, m_out, workspace, chunk:
     hqc_decrypt_host_workspace_bytes(level, chunk) bytes."""
     p = params(level)
     B = _rows(u, 8 * p.u_stride, "u")
-    assert _rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B
-    assert _rows(m_out, p.k, "m_out") == B
+    _need(_rows(v, 8 * p.v_words, "v") == B and _rows(y_support, 4 * p.y_stride, "y") == B, "row counts of the arguments disagree")
+    _need(_rows(m_out, p.k, "m_out") == B, "row counts of the arguments disagree")
     wb = workspace.numel() * workspace.element_size()
     _check(lib().hqc_decrypt_batch_host(ctypes.byref(_cp(level)), _hptr(u), _hptr(v), _hptr(y_support), _hptr(m_out),
                                         B, _ptr(workspace), wb, chunk, _stream(stream)))
@@ -319,10 +376,9 @@ def hqc_decrypt_ct_batch_host(level: int, ct, key_index, y_keys, m_out, workspac
     is one key) in, host m out; y_keys is the device-resident [nkeys][y_stride] key-support table."""
     p = params(level)
     B = _rows(ct, hqc_ct_bytes(level), "ct")
-    assert _rows(m_out, p.k, "m_out") == B
+    _need(_rows(m_out, p.k, "m_out") == B, "row counts of the arguments disagree")
     nk = _rows(y_keys, 4 * p.y_stride, "y_keys")
-    if key_index is not None:
-        assert _rows(key_index, 4, "key_index") == B
+    _keys_in_range(key_index, nk, B, True) if key_index is not None else _need(nk >= 1, "y_keys: at least one key")
     wb = workspace.numel() * workspace.element_size()
     _check(lib().hqc_decrypt_ct_batch_host(ctypes.byref(_cp(level)), _hptr(ct),
                                            None if key_index is None else _hptr(key_index), _ptr(y_keys), nk,

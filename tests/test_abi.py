@@ -100,3 +100,33 @@ def test_binding_refuses_cpu_tensors(L):
     x = torch.zeros(64, dtype=torch.uint8)
     with pytest.raises(hqc.HqcError):
         hqc.hqc_rm_decode_batch(1, x, x)
+
+
+def test_helper_and_key_index_validation(L):
+    """ABI checks added in round 2: the helpers check pointer alignment like
+    every entry point; the serialized-ciphertext call rejects a HOST key index >= nkeys with HQC_ERR_SIZE
+    before anything is enqueued (it used to clamp it); the binding raises HqcError (not assert) on
+    mismatched row counts, so python -O keeps the checks."""
+    P = hqc._Params
+    p = P()
+    L.hqc_get_params(1, ctypes.byref(p))
+    a16, a8 = ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1008)
+    cnt = ctypes.c_void_p(0x2000)
+    assert L.hqc_count_mismatch(ctypes.byref(p), a8, a16, 4, cnt, None) == -3
+    assert L.hqc_count_mismatch(ctypes.byref(p), a16, a16, 4, ctypes.c_void_p(0x2008), None) == -3
+    assert L.hqc_count_mismatch(ctypes.byref(p), a16, None, 4, cnt, None) == -2
+    assert L.hqc_validate_support(ctypes.byref(p), a8, 4, cnt, None) == -3
+    assert L.hqc_validate_support(ctypes.byref(p), a16, 4, None, None) == -2
+    keys = (ctypes.c_uint32 * 4)(0, 1, 2, 1)
+    ws = L.hqc_decrypt_ct_host_workspace_bytes(ctypes.byref(p), 4)
+    assert L.hqc_decrypt_ct_batch_host(ctypes.byref(p), a16, keys, a16, 2, a16, 4, a16, ws, 4, None) == -4
+    torch = pytest.importorskip("torch")
+    ct = torch.zeros(2 * 4417, dtype=torch.uint8)
+    m = torch.zeros(3 * 16, dtype=torch.uint8)
+    with pytest.raises(hqc.HqcError):  # 2 ciphertexts, 3 output rows: refused before the C call
+        hqc.hqc_decrypt_ct_batch_host(1, ct, None, torch.zeros(4 * p.y_stride, dtype=torch.uint8), m,
+                                      torch.zeros(16, dtype=torch.uint8))
+    with pytest.raises(hqc.HqcError):  # host key index out of range
+        hqc.hqc_decrypt_ct_batch_host(1, ct, torch.tensor([0, 5], dtype=torch.int32).view(torch.uint8),
+                                      torch.zeros(4 * p.y_stride, dtype=torch.uint8), m[:32],
+                                      torch.zeros(16, dtype=torch.uint8))

@@ -68,6 +68,64 @@ def test_encrypt_matches_oracle(level):
     assert (gv == W["v"]).all()
 
 
+def _edge_rows(sup, n, w):
+    """Supports that reach the top of the doubled operand: position 0 (rotation d = n), n - 1 (d = 1), the
+    run n-1, n-2, ... and the run 0, 1, ...; the other rows keep their generator draws."""
+    sup = sup.copy()
+    for i in range(sup.shape[0]):
+        kind = i % 5
+        row = np.sort(sup[i, :w])
+        if kind == 0:
+            row[0] = 0 if 0 not in row else row[0]
+        elif kind == 1:
+            row[-1] = n - 1 if n - 1 not in row else row[-1]
+        elif kind == 2:
+            row = (n - 1 - np.arange(w)).astype(np.uint32)
+        elif kind == 3:
+            row = np.arange(w, dtype=np.uint32)
+        else:
+            row[0], row[-1] = (0 if 0 not in row else row[0]), (n - 1 if n - 1 not in row else row[-1])
+        assert len(set(row.tolist())) == w
+        sup[i, :w] = row
+    return sup
+
+
+@pytest.mark.parametrize("kernel", ["1", "2"])
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_encrypt_and_keygen_edge_supports(level, kernel, monkeypatch):
+    """Encrypt (both kernels: HQC_ENC_KERNEL, read per call) with r1, r2, e supports containing 0, n-1 and
+    the runs at either end, and the KeyGen product with such x, y: the windows that reach the top word of
+    the doubled operand. Bit-exact against the oracle."""
+    monkeypatch.setenv("HQC_ENC_KERNEL", kernel)
+    p, g, sh = oracle.params(level), hqc.params(level), shape_for(level)
+    W = valid_batch(level, 30_000, 40)
+    for key in ("r1", "r2", "e"):
+        W[key] = _edge_rows(W[key], p.n, p.wr)
+    H = np.zeros((W["h"].shape[0], g.u_stride), np.uint64)
+    H[:, : W["h"].shape[1]] = W["h"]
+    S = np.zeros_like(H)
+    S[:, : p.words] = W["s"]
+    key = W["key"].astype(np.uint32)
+    B = 40
+    u = torch.empty(B * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    v = torch.empty(B * g.v_words * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_encrypt_batch(level, dev(H), dev(S), dev(key), dev(W["m"]), dev(W["r1"]), dev(W["r2"]), dev(W["e"]), u, v)
+    torch.cuda.synchronize()
+    gu, gv = host(u, np.uint64, g.u_stride), host(v, np.uint64, g.v_words)
+    for i in range(B):
+        k = key[i]
+        ou, ov = oracle.encrypt(p, W["h"][k], W["s"][k], W["m"][i], W["r1"][i], W["r2"][i], W["e"][i])
+        assert (gu[i, : p.words] == ou).all() and (gu[i, p.words:] == 0).all() and (gv[i] == ov).all(), i
+    # KeyGen product s = x + h * y with edge supports in x and y
+    h, x, y = gen.key_draws(0xED6E, sh, 0, 10)
+    x, y = _edge_rows(x, p.n, p.w), _edge_rows(y, p.n, p.w)
+    s = torch.empty(10 * g.u_stride * 8, dtype=torch.uint8, device=DEV)
+    hqc.hqc_keygen_batch(level, dev(h), dev(x), dev(y), s)
+    torch.cuda.synchronize()
+    ref = np.stack([oracle.keygen(p, h[i, : p.words], x[i], y[i]) for i in range(10)])
+    assert (host(s, np.uint64, g.u_stride)[:, : p.words] == ref).all()
+
+
 @pytest.mark.parametrize("level,B", [(3, 65536)])
 def test_gpu_encrypt_decrypt_round_trip_full_size(level, B):
     """configs[1] at full size entirely on the device: GPU keygen + encrypt of generator draws, then the

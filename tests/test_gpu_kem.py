@@ -109,8 +109,9 @@ def test_decaps_matches_oracle_with_implicit_rejection(level):
         elif kind[i] == 2:  # one bit of v: rejected
             b = int(rng.integers(p.n12))
             V[i, b // 64] ^= np.uint64(1) << np.uint64(b % 64)
-        elif kind[i] == 3:  # a bit of u in [n, 8*ceil(n/8)) or in the padding: accepted (ignored by
-            b = p.n + int(rng.integers(64 * g.u_stride - p.n))  # the compare), K follows the bytes
+        elif kind[i] == 3:  # a bit of u in [n, 8*ceil(n/8)) (inside the serialized bytes: rejected)
+            ub = 8 * ((p.n + 7) // 8)  # or beyond them in the row's padding (not part of c: accepted)
+            b = p.n + int(rng.integers(ub - p.n)) if (i // 6) % 2 == 0 else ub + int(rng.integers(64 * g.u_stride - ub))
             U[i, b // 64] ^= np.uint64(1) << np.uint64(b % 64)
         elif kind[i] == 4:  # uniformly random ciphertext
             U[i, : p.words] = rng.integers(0, 2**63, p.words, dtype=np.uint64)
@@ -119,6 +120,8 @@ def test_decaps_matches_oracle_with_implicit_rejection(level):
             V[i] = V[(i + 1) % B]
     Kref, accref = oracle.kem_decaps_batch(p, H, S, hpk, sigma, key.astype(np.int64), y[key], U, V)
     assert accref[kind == 0].all() and not accref[(kind == 1) | (kind == 2) | (kind == 4)].any()
+    k3 = np.nonzero(kind == 3)[0]
+    assert not accref[k3[(k3 // 6) % 2 == 0]].any() and accref[k3[(k3 // 6) % 2 == 1]].all()
     K, acc = empty(B * 64), empty(B)
     ws = empty(hqc.hqc_kem_workspace_bytes(level, B))
     Y = np.zeros((nk, g.y_stride), np.uint32)

@@ -267,10 +267,11 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
-    """The library picks the warp-pair kernel (HQC-3) or the one-warp kernel (HQC-1/5) per level; the
-    warp-specialised kernel (3) and the tensor-memory-product kernel (4) are alternatives. HQC_DEC_KERNEL
+    """The library picks the warp-pair kernel (HQC-3) or the one-warp kernel (HQC-1/5) per level, and the
+    small-batch group kernel (5) for small batches; the warp-specialised kernel (3) and the
+    tensor-memory-product kernel (4) are alternatives. HQC_DEC_KERNEL
     forces each (read once per process), so each runs in a subprocess on every level."""
     import subprocess
     import sys
@@ -472,3 +473,37 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+# ---------------------------------------------------------------- small batches (K4s) and split launches
+@pytest.mark.parametrize("level,B", [(1, 1), (1, 33), (1, 1024), (3, 1), (3, 33), (3, 1024), (5, 1), (5, 33),
+                                     (5, 1024)])
+def test_small_batch_kernel(level, B):
+    """BASELINE configs[0]'s size class: batches up to SMs x 8 take k_decrypt_sb (groups of G ciphertexts,
+    one warp each, G chosen to spread the batch over all SMs). Bit-exact against the oracle,
+    with a quarter of the rows replaced by uniformly random (undecodable) ciphertexts."""
+    W = valid_batch(level, 90_000, B)
+    p = W["params"]
+    nr = B // 4
+    if nr:
+        W["u"][:nr] = gen.dense(41, gen.TAG_U_RAND, 0, nr, p.n, W["u"].shape[1])
+        W["v"][:nr] = gen.dense(41, gen.TAG_V_RAND, 0, nr, p.n12, W["v"].shape[1])
+    grid, wpc = hqc.hqc_decrypt_launch_shape(level, B)
+    assert grid * wpc >= B and grid <= torch.cuda.get_device_properties(DEV).multi_processor_count
+    got = gpu_decrypt(level, W)
+    assert (got == oracle.decrypt_batch(p, W["u"], W["v"], W["y"])).all()
+    assert (got[nr:] == W["m"][nr:]).all()
+
+
+@pytest.mark.parametrize("sb_max,split", [("100000", ""), ("0", "700"), ("0", "64")])
+def test_group_striding_and_split_launches(sb_max, split, monkeypatch):
+    """Launch policies read on every call: HQC_SB_MAX forces k_decrypt_sb on a batch larger than its grid
+    (groups strided over the CTAs), HQC_DEC_SPLIT runs one batch as consecutive launches of at most that
+    many ciphertexts (ragged last launch); HQC-1 adversarial rows, compared with the oracle."""
+    W = adversarial_batch(0, 3000, 3000)
+    p = W["params"]
+    ref = oracle.decrypt_batch(p, W["u"], W["v"], W["y"])
+    monkeypatch.setenv("HQC_SB_MAX", sb_max)
+    monkeypatch.setenv("HQC_DEC_SPLIT", split)
+    got = gpu_decrypt(1, W)
+    assert (got == ref).all()

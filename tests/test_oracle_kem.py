@@ -97,6 +97,14 @@ def test_round_trip_and_implicit_rejection(level):
         assert not ok3
         assert K3 == hashlib.shake_256(sigma.tobytes() + _ser(p, u2, v2) + b"\x03").digest(64)
         assert K3 == oracle.kem_decaps(p, h, s, hpk, y, sigma, u2, v2)[0]  # deterministic
+        # a bit of u in [n, 8 ceil(n/8)) is inside the serialized c, so c' != c byte-wise:
+        # rejected, and K hashes the received bytes
+        b = p.n + t % (8 * ((p.n + 7) // 8) - p.n)
+        u4 = u.copy()
+        u4[b // 64] ^= np.uint64(1) << np.uint64(b % 64)
+        K4, ok4 = oracle.kem_decaps(p, h, s, hpk, y, sigma, u4, v)
+        assert not ok4 and _ser(p, u4, v) != _ser(p, u, v)
+        assert K4 == hashlib.shake_256(sigma.tobytes() + _ser(p, u4, v) + b"\x03").digest(64)
 
 
 def test_decaps_batch_matches_single():
