@@ -22,23 +22,24 @@ def main():
     ap.add_argument("--level", type=int, default=3)
     ap.add_argument("--batch", type=int, default=65536)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--only", default="all", choices=["all", "fused", "s1", "s2", "s3"])
+    ap.add_argument("--only", default="all", choices=["all", "fused", "s1", "s1n", "s2", "s3"])
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     p = hqc.params(a.level)
     B = a.batch
     u, v, y = make_inputs(a.level, 0, B, p)
-    du, dv, dy = (torch.from_numpy(x.view(np.uint8)).to(dev) for x in (u, v, y))
+    du, dv, dy = (torch.from_numpy(x.view(np.uint8).reshape(-1)).to(dev) for x in (u, v, y))
     dm = torch.empty(B * p.k, dtype=torch.uint8, device=dev)
     dr = torch.empty(B * p.v_words * 8, dtype=torch.uint8, device=dev)
     ds = torch.empty(B * p.n1, dtype=torch.uint8, device=dev)
     ops = {
         "fused": lambda: hqc.hqc_decrypt_batch(a.level, du, dv, dy, dm),
         "s1": lambda: hqc.hqc_sparse_dense_mul_batch(a.level, du, dy, dv, dr),
+        "s1n": lambda: hqc.hqc_sparse_dense_mul_batch(a.level, du, dy, None, dr),  # standalone product, v = NULL
         "s2": lambda: hqc.hqc_rm_decode_batch(a.level, dr, ds),
         "s3": lambda: hqc.hqc_rs_decode_batch(a.level, ds, dm),
     }
-    names = list(ops) if a.only == "all" else [a.only]
+    names = [n for n in ops if n != "s1n"] if a.only == "all" else [a.only]
     if a.only in ("s2", "s3"):
         ops["s1"]()
         if a.only == "s3":
