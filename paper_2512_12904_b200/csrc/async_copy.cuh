@@ -48,4 +48,19 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
+// 1-D TMA bulk store shared -> global (SASS UBLKCP), tracked by a per-thread bulk group: the issuing
+// thread commits it and later waits until the source has been READ (the buffer may then be rewritten)
+// or, before the kernel exits, until it has been read as well (shared memory must outlive the read).
+// bytes: multiple of 16; dst/src 16-byte aligned. The generic-proxy writes to src must be ordered
+// before it with fence_proxy_async_smem() by the writing threads (and a __syncwarp).
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 }  // namespace hqc

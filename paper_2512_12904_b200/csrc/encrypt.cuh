@@ -12,6 +12,7 @@
 #pragma once
 #include <cstdint>
 
+#include "async_copy.cuh"
 #include "gf256.cuh"
 #include "levels.cuh"
 #include "stage1.cuh"
@@ -283,10 +284,13 @@ template <class P> struct Enc2Smem {
   static constexpr uint32_t OUT_WORDS = 2 * P::U_STRIDE > P::NW ? 2 * P::U_STRIDE : P::NW;
   static constexpr uint32_t OUT_BYTES = round_up(OUT_WORDS * 4, 16);
   static constexpr uint32_t SUP_BYTES = round_up(P::E_STRIDE * 4, 16);
+  static_assert((P::E_STRIDE * 4) % 16 == 0, "support rows are TMA bulk copies");
   static constexpr uint32_t D_BYTES = round_up(round_up(P::WR, 4) * 4, 16);
   static constexpr uint32_t MISC_BYTES = round_up(P::N1 + P::K + 16, 16);
-  static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + 2 * SUP_BYTES + D_BYTES;
-  static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + 2 * SUP_BYTES + D_BYTES + MISC_BYTES;
+  // two buffers of (r2 row, r1 or e row), prefetched by TMA one ciphertext ahead; two mbarriers
+  static constexpr uint32_t SUPS_BYTES = 4 * SUP_BYTES + 16;
+  static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + SUPS_BYTES + D_BYTES;
+  static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + SUPS_BYTES + D_BYTES + MISC_BYTES;
   static constexpr uint32_t BYTES = W0_BYTES + W1_BYTES;
 };
 
@@ -308,27 +312,61 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
   uint8_t *base = smem + (wid ? M::W0_BYTES : 0u);
   uint32_t *E = reinterpret_cast<uint32_t *>(base);
   uint32_t *out = reinterpret_cast<uint32_t *>(base + (wid ? M::EV_BYTES : M::EU_BYTES));
-  uint32_t *s_r2 = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(out) + M::OUT_BYTES);
-  uint32_t *s_x = s_r2 + M::SUP_BYTES / 4;  // r1 (warp 0) or e (warp 1)
-  uint32_t *dsm = s_x + M::SUP_BYTES / 4;
+  uint32_t *sups = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(out) + M::OUT_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sups) + 4 * M::SUP_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(sups) + M::SUPS_BYTES);
   uint8_t *cw = reinterpret_cast<uint8_t *>(dsm) + M::D_BYTES;  // warp 1 only
   uint8_t *msg = cw + P::N1;
   const size_t lo = (size_t)blockIdx.x * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
+  const uint32_t *xsrc = wid ? e : r1;  // r1 (warp 0) or e (warp 1)
+  constexpr uint32_t SB = P::E_STRIDE * 4;
+  // buffer b: r2 row at sups + 2 b SUP, the r1 / e row at sups + (2 b + 1) SUP; mbarrier bar[b]
+  auto sup_r2 = [&](int b) { return sups + (2 * b) * (M::SUP_BYTES / 4); };
+  auto sup_x = [&](int b) { return sups + (2 * b + 1) * (M::SUP_BYTES / 4); };
+  auto prefetch = [&](size_t c, int b) {  // the supports of ciphertext c, one ciphertext ahead
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar + b, 2 * SB);
+      tma_load_1d(sup_r2(b), r2 + c * P::E_STRIDE, SB, bar + b);
+      tma_load_1d(sup_x(b), xsrc + c * P::E_STRIDE, SB, bar + b);
+    }
+  };
+  // the previous ciphertext's output store (TMA, async) must have read `out` before it is rewritten
+  auto out_free = [&]() {
+    if (!CMP && lane == 0) tma_store_wait_read();
+    __syncwarp();
+  };
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncwarp();
+  uint32_t ph0 = 0, ph1 = 0;
+  uint32_t mnext = (wid && lo < hi && (uint32_t)lane < P::K) ? m[lo * P::K + lane] : 0u;
+  if (lo < hi) prefetch(lo, 0);
   size_t cached = ~(size_t)0;
   for (size_t ct = lo; ct < hi; ct++) {
+    const int b = (int)((ct - lo) & 1);
     const size_t key = key_index ? key_index[ct] : ct;
     if (key != cached) {  // a public index: the only data-dependent branch, on public data
+      out_free();
       copy_g2s(out, (wid ? s : h) + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
       __syncwarp();
       if (wid) s1_build_E<P, typename M::SV>(out, E, lane);
       else s1_build_E<P, typename M::SU>(out, E, lane);
       cached = key;
     }
-    copy_g2s(s_r2, r2 + ct * P::E_STRIDE, P::E_STRIDE, lane);
-    copy_g2s(s_x, (wid ? e : r1) + ct * P::E_STRIDE, P::E_STRIDE, lane);
-    if (wid)
-      for (uint32_t j = lane; j < P::K; j += 32) msg[j] = m[ct * P::K + j];
+    if (wid) {  // this ciphertext's message (loaded one ciphertext ahead), then the next one's
+      if ((uint32_t)lane < P::K) msg[lane] = (uint8_t)mnext;
+      mnext = (ct + 1 < hi && (uint32_t)lane < P::K) ? m[(ct + 1) * P::K + lane] : 0u;
+    }
+    mbar_wait(bar + b, b ? ph1 : ph0);
+    if (b) ph1 ^= 1u; else ph0 ^= 1u;
+    __syncwarp();  // every lane has seen the rows land (and is done with buffer b ^ 1 of ciphertext ct - 1)
+    if (ct + 1 < hi) prefetch(ct + 1, b ^ 1);
+    const uint32_t *s_r2 = sup_r2(b);
+    uint32_t *s_x = sup_x(b);
     __syncwarp();
     uint32_t diff = 0;
     if (wid == 0) {  // u = r1 + h * r2 (all n bits)
@@ -337,6 +375,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       __syncwarp();
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
+      out_free();
       s1_store_r<S>(acc, out, lane);
       if constexpr (enc_tail<P>() != 0) {
         uint32_t t[enc_tail<P>()];
@@ -355,8 +394,10 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
           const uint32_t x = q < P::Q0 ? uc[q] : (q == P::Q0 ? uc[q] & P::CB_MASK : 0u);
           diff |= x ^ out[q];
         }
-      } else {
-        copy_s2g(u_out + ct * P::U_STRIDE, out, 2 * P::U_STRIDE, lane);
+      } else {  // u row to HBM by a TMA bulk store; `out` is rewritten only after out_free()
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tma_store_1d(u_out + ct * P::U_STRIDE, out, P::U_STRIDE * 8);
       }
     } else {  // v = trunc(mG + s * r2 + e)
       using S = typename M::SV;
@@ -365,6 +406,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       __syncwarp();
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
+      out_free();
       s1_store_r<S>(acc, out, lane);
       if constexpr (enc_tail_v<P>() != 0) {
         uint32_t t[enc_tail_v<P>()];
@@ -392,7 +434,9 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
           diff |= (x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w);
         }
       } else {
-        copy_s2g(v_out + ct * P::V_WORDS, out, P::NW, lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tma_store_1d(v_out + ct * P::V_WORDS, out, P::V_WORDS * 8);
       }
     }
     if constexpr (CMP) {
@@ -401,6 +445,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
     }
     __syncwarp();
   }
+  if (!CMP && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
 }
 
 }  // namespace hqc

@@ -162,12 +162,14 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA_S1, HQC_S1K_MINB) k_stage1(
   size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (ct < batch) pipe.issue_uy(ct, lane);
   for (; ct < batch; ct += nwarps) {
-    pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
-    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
-    const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E);
-    for (uint32_t c = lane; c < P::NW / 4; c += 32) dst[c] = src[c];
+    if (lane == 0) tma_store_wait_read();  // the previous r (in E) has been read by its store
     __syncwarp();
+    pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
+    fence_proxy_async_smem();  // r (in E) -> HBM by a TMA bulk store, asynchronous to the next product
+    __syncwarp();
+    if (lane == 0) tma_store_1d(r_out + ct * P::V_WORDS, pipe.E, P::V_WORDS * 8);
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // E built up to E_WORDS words (an E-build shape with the pair's E size)
@@ -242,13 +244,16 @@ __global__ void __launch_bounds__(64, 1) k_stage1p(const uint64_t *__restrict__ 
     } else {
       s1_store_r<S>(acc, E + wid * M::NWH, lane);
     }
+    fence_proxy_async_smem();
     __syncthreads();
-    uint4 *dst = reinterpret_cast<uint4 *>(r_out + ct * P::V_WORDS);
-    const uint4 *src = reinterpret_cast<const uint4 *>(E);
-    for (uint32_t c = tid; c < P::NW / 4; c += 64) dst[c] = src[c];
+    if (tid == 0) {  // r (in E) -> HBM by a TMA bulk store; E is rebuilt only after it has been read
+      tma_store_1d(r_out + ct * P::V_WORDS, E, P::V_WORDS * 8);
+      if (v && next < batch) issue_uy(next);
+      tma_store_wait_read();
+    }
     __syncthreads();  // E and the staging buffer are free again
-    if (v && tid == 0 && next < batch) issue_uy(next);
   }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // K2: stage 2 alone. One thread per RM block.
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
                                                                         const uint64_t *__restrict__ v,
                                                                         const uint32_t *__restrict__ y,
                                                                         uint8_t *__restrict__ m_out,
-                                                                        size_t batch) {
+                                                                        size_t batch, uint32_t stagger_ns) {
   using M = SbSmem<P>;
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);
@@ -405,6 +410,7 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
   if (ct < batch) pipe.issue_uy(ct, lane);  // the first rows are in flight while the GF tables are copied
   gf_tables_to_smem(gf);
   __syncthreads();
+  if (stagger_ns) __nanosleep(stagger_ns * (uint32_t)wib);  // experiments: de-phase the warps of a CTA
   PHASE(0);
   for (; ct < batch; ct += step) {
     pipe.run(ct, ct + step < batch, ct + step, lane);
@@ -1025,7 +1031,8 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       k_decrypt_t<P><<<grid, 32 * TmDec<P>::WARPS, decrypt_t_smem<P>(), st>>>(u, v, y, m, batch, per);
       break;
     case 5:
-      k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
+          u, v, y, m, batch, (uint32_t)env_long("HQC_SB_STAGGER", 0));
       break;
     default: k_decrypt_ws<P><<<grid, 128, decrypt_ws_smem<P>(), st>>>(u, v, y, m, batch, per); break;
   }

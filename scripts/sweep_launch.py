@@ -84,6 +84,21 @@ if __name__ == "__main__":
         small([1, 3, 5], [1, 8, 33, 148, 296, 512, 1024, 1184, 2048, 4096, 8192, 16384])
     elif what == "large":
         small([1, 3, 5], [32768, 65536, 262144])
+    elif what == "stagger":
+        dev = torch.device("cuda:0")
+        cases = [tuple(map(int, c.split(":"))) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
+            [(3, 65536), (3, 262144), (1, 16384)]
+        for level, B in cases:
+            p = hqc.params(level)
+            u, v, y = (torch.from_numpy(a.view(np.uint8).reshape(-1)).to(dev) for a in bench.make_inputs(level, 0, B, p))
+            m = torch.empty(B * p.k, dtype=torch.uint8, device=dev)
+            run = lambda: hqc.hqc_decrypt_batch(level, u, v, y, m)  # noqa: E731
+            for ns in (0, 250, 500, 1000, 2000, 4000):
+                os.environ["HQC_SB_STAGGER"] = str(ns)
+                run()
+                ms = graph_ms(run) if B <= 16384 else bench._timed_ms(run, 10)
+                print(json.dumps({"level": level, "B": B, "stagger_ns": ns, "ms": ms, "rate": B / ms * 1e3}), flush=True)
+            os.environ.pop("HQC_SB_STAGGER")
     elif what == "split":
         B = int(sys.argv[2]) if len(sys.argv) > 2 else 4_194_304
         split([1, 3, 5], B, [0, 32768, 65536, 131072, 262144, 524288, 1048576])
