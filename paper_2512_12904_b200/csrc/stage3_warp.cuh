@@ -17,11 +17,20 @@
 #pragma once
 #include <cstdint>
 
+#include "exp_timing.cuh"
 #include "gf256.cuh"
 #include "levels.cuh"
 #include "stage3.cuh"
 
 namespace hqc {
+
+// Berlekamp–Massey with the discrepancy formed one iteration ahead (a shorter dependent chain, more
+// instructions): BM 6.4k -> 5.4k cycles per HQC-1 word; configs[0] (HQC-1, 1,024) 18.1 -> 17.7 us, but
+// HQC-3 at 65,536 (where k_decrypt_sb runs throughput-bound) 1.175 -> 1.198 ms (profiles/r02/ab_bm.log).
+// So per level: on where K4s serves only small, latency-bound batches (HQC-1, HQC-5), off for HQC-3.
+#ifndef HQC_BM_LOOKAHEAD
+#define HQC_BM_LOOKAHEAD (P::level != 3)
+#endif
 
 // Per-warp scratch (uint16 logs): log sym_j (n1), a sentinel pad of delta+1 rows then log S_{i+1} (2delta),
 // log Lambda_t (delta+1), log Omega_i (2delta).
@@ -44,6 +53,7 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   const uint8_t *EXPT = gf->exp;
   const uint16_t *LOGT = gf->log;
   uint16_t *lsym = scr + W::LSYM, *lS = scr + W::LS, *lLam = scr + W::LLAM, *lOm = scr + W::LOM;
+  PHASE_T0();
   for (int j = lane; j < N1; j += 32) lsym[j] = LOGT[sym[j]];
   for (int t = lane; t < (int)W::PAD; t += 32) lS[t - (int)W::PAD] = GF_LOG0;  // log S_i for i <= 0
   __syncwarp();
@@ -68,12 +78,44 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
       if (lane + 32 * q < TD) lS[lane + 32 * q] = LOGT[s[q]];
   }
   __syncwarp();
+  PHASE(9);
 
   // ---- Berlekamp–Massey: lane t <= delta holds Lambda_t and log (x^m B)_t
   const bool coef = lane <= DL;
   uint32_t lam = lane == 0 ? 1u : 0u;
   uint32_t lbx = lane == 1 ? 0u : GF_LOG0;  // Bx = x * 1
   uint32_t L = 0, lb = 0;
+  if constexpr (HQC_BM_LOOKAHEAD) {
+  // The discrepancy of iteration r+1 is formed from iteration r's quantities, so that its dependent chain
+  // is lc -> one product -> REDUX -> log, not lc -> update Lambda -> log Lambda -> product -> REDUX -> log:
+  //   d_{r+1} = sum_t Lambda'_t S_{r+2-t},  Lambda' = Lambda + c x^m B   (c = d_r / b, log c = lc)
+  //           = XOR_t [ Lambda_t S_{r+2-t} ]  XOR  [ c (x^m B)_t S_{r+2-t} ]
+  // The first part only needs log Lambda_t of iteration r (known before lc); the update of Lambda and its
+  // log run beside the chain. Same values as the plain recurrence (GF arithmetic is exact).
+  uint32_t llam = LOGT[lam];
+  uint32_t d = __reduce_xor_sync(0xffffffffu, coef ? EXPT[llam + lS[-lane]] : 0u);  // d_0 = S_1
+  uint32_t ld = LOGT[d];
+#pragma unroll 1
+  for (int r = 0; r < TD; r++) {
+    // log S_{r+2-t}; at r = 2delta-1 lane 0 reads the row past the syndromes (not yet written): its d is
+    // never used, and the clamp keeps every table index below 1024
+    const uint32_t lsn = min((uint32_t)lS[r + 1 - lane], GF_LOG0);
+    const uint32_t partA = coef ? EXPT[llam + lsn] : 0u;    // Lambda_t S_{r+2-t}
+    const uint32_t lc = d ? mod255_sub(ld, lb) : GF_LOG0;  // log(d / b)
+    const bool grow = (d != 0) && (2 * L <= (uint32_t)r);
+    const bool zc = lc == GF_LOG0 || lbx == GF_LOG0;
+    const uint32_t lcb = mod255_add(zc ? 0u : lc, zc ? 0u : lbx);  // log (c (x^m B)_t)
+    const uint32_t partB = (coef && !zc) ? EXPT[lcb + lsn] : 0u;
+    lam ^= (coef && !zc) ? EXPT[lcb] : 0u;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, grow ? llam : lbx, 1);
+    lbx = (lane == 0 || !coef) ? GF_LOG0 : up;
+    L = grow ? (uint32_t)r + 1 - L : L;
+    lb = grow ? ld : lb;
+    d = __reduce_xor_sync(0xffffffffu, partA ^ partB);  // d_{r+1} (the last one is not used)
+    ld = LOGT[d];
+    llam = LOGT[lam];
+  }
+  } else {
 #pragma unroll 1
   for (int r = 0; r < TD; r++) {
     const uint32_t llam = LOGT[lam];
@@ -88,10 +130,12 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     L = grow ? (uint32_t)r + 1 - L : L;
     lb = grow ? ld : lb;
   }
+  }
   const uint32_t nzmask = __ballot_sync(0xffffffffu, coef && lam != 0);
   const uint32_t deg = 31u - __clz(nzmask);  // Lambda_0 = 1 always
   if (coef) lLam[lane] = LOGT[lam];
   __syncwarp();
+  PHASE(10);
 
   // ---- Chien search over j < n1 (lane j + 32 q); the odd part of Lambda(alpha^-j) kept for j < k
   uint32_t nroots = 0, root_mine = 0, lodd_mine = GF_LOG0;
@@ -114,6 +158,7 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     }
   }
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
+  PHASE(11);
 
   // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta
 #pragma unroll
@@ -125,6 +170,7 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     if (i < TD) lOm[i] = LOGT[om];
   }
   __syncwarp();
+  PHASE(12);
 
   // ---- Forney on message position j = lane < k: e_j = Omega(alpha^-j) / (alpha^j Lambda_odd(alpha^-j))
   if (lane < K) {
@@ -141,6 +187,7 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     const uint32_t fix = (ok && root_mine) ? ej : 0u;
     if (out != nullptr) out[lane] = (uint8_t)(sym[lane] ^ fix);
   }
+  PHASE(13);
   return ok ? 1u : 0u;
 }
 

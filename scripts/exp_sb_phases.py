@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 SO = os.path.join(ROOT, "scripts", "libhqc_exp_timing.so")
 PH = ["prologue", "run.wait_uy", "run.stage_d+build_E", "run.product", "run.wait_v+store", "stage2", "-",
-      "rs_decode_warp"]
+      "rs_decode_warp", "-", "rs.syndromes", "rs.bm", "rs.chien", "rs.omega", "rs.forney"]
 
 
 def build():

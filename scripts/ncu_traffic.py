@@ -27,11 +27,10 @@ def metrics(rep):
                 dram_write=val("dram__bytes_write.sum"), duration_ns=ns)
 
 
-def main(out, reps):
+def main(out, reps, batches=(65536, 65536, 65536)):
     res = {}
-    for level, rep in zip((1, 3, 5), reps):
+    for level, rep, batch in zip((1, 3, 5), reps, batches):
         m = metrics(rep)
-        batch = 65536
         m.update(level=level, batch=batch, bytes_per_decryption=(m["dram_read"] + m["dram_write"]) / batch,
                  report=os.path.basename(rep))
         res[str(level)] = m
@@ -40,4 +39,5 @@ def main(out, reps):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2:5])
+    main(sys.argv[1], sys.argv[2:5], tuple(int(b) for b in sys.argv[5].split(",")) if len(sys.argv) > 5 else
+         (65536, 65536, 65536))
