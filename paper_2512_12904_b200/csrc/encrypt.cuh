@@ -68,6 +68,70 @@ __device__ __forceinline__ void rs_encode_warp(const uint8_t *msg, uint8_t *cw, 
   if ((uint32_t)lane + 32 < TD) cw[P::N1 - 1 - (lane + 32)] = (uint8_t)B;
 }
 
+// The same encoder on byte-wide log/antilog tables in SHARED memory (k_encrypt2): the product g*_t * fb
+// becomes EXP8[log fb + log g*_t], log g*_t a per-lane constant. The product table above lives in global
+// memory (8-15 KB, too large for the shared-memory budget of k_encrypt2) and each of the k dependent steps
+// waited on an L1/L2 load: 7% of k_encrypt2's stall samples at HQC-3 (profiles/r02/ncu_encrypt.md).
+struct Gf8Tables {
+  uint8_t log[256];  // log_alpha(x), 255 for x = 0
+  uint8_t exp[512];  // alpha^(e mod 255) for e < 510; 0 for 510, 511
+};
+constexpr Gf8Tables make_gf8_tables() {
+  Gf8Tables t{};
+  uint32_t x = 1;
+  for (uint32_t e = 0; e < 255; e++) {
+    t.exp[e] = t.exp[e + 255] = static_cast<uint8_t>(x);
+    t.log[x] = static_cast<uint8_t>(e);
+    x = gf_mul_c(x, 2);
+  }
+  t.log[0] = 255;
+  return t;
+}
+__device__ __align__(16) const Gf8Tables g_gf8 = make_gf8_tables();
+static_assert(sizeof(Gf8Tables) % 16 == 0, "copied in 16-byte pieces");
+
+template <uint32_t TD> struct RsGenLog {
+  uint8_t lg[64];  // log g*_t for t < TD (255 for a zero coefficient), 255 beyond
+};
+template <uint32_t TD> constexpr RsGenLog<TD> make_rs_gen_log() {
+  RsGenLog<TD> L{};
+  const RsEncTable<TD> T = make_rs_enc_table<TD>();  // T[1][t] = g*_t
+  const Gf8Tables g = make_gf8_tables();
+  for (uint32_t t = 0; t < 64; t++) L.lg[t] = t < TD ? g.log[T.t[1][t]] : 255;
+  return L;
+}
+__device__ const RsGenLog<30> g_rs_lg30 = make_rs_gen_log<30>();
+__device__ const RsGenLog<32> g_rs_lg32 = make_rs_gen_log<32>();
+__device__ const RsGenLog<58> g_rs_lg58 = make_rs_gen_log<58>();
+template <uint32_t TD> __device__ __forceinline__ const uint8_t *rs_gen_log();
+template <> __device__ __forceinline__ const uint8_t *rs_gen_log<30>() { return g_rs_lg30.lg; }
+template <> __device__ __forceinline__ const uint8_t *rs_gen_log<32>() { return g_rs_lg32.lg; }
+template <> __device__ __forceinline__ const uint8_t *rs_gen_log<58>() { return g_rs_lg58.lg; }
+
+__device__ __forceinline__ uint32_t gf8_mul_log(const Gf8Tables *t, uint32_t la, uint32_t lb) {
+  return (la == 255u || lb == 255u) ? 0u : t->exp[la + lb];
+}
+
+template <class P>
+__device__ __forceinline__ void rs_encode_warp_log(const uint8_t *msg, uint8_t *cw, const Gf8Tables *g, int lane) {
+  constexpr uint32_t TD = P::TWO_DELTA;
+  const uint8_t *LG = rs_gen_log<TD>();
+  const uint32_t lgA = __ldg(LG + lane), lgB = __ldg(LG + 32 + lane);  // 255 beyond TD
+  uint32_t A = 0, B = 0;  // cells lane and lane + 32
+  for (uint32_t j = 0; j < P::K; j++) {
+    const uint32_t top = (TD - 1 < 32) ? __shfl_sync(0xffffffffu, A, TD - 1) : __shfl_sync(0xffffffffu, B, TD - 1 - 32);
+    const uint32_t lf = g->log[msg[j] ^ top];  // one address for the whole warp: a broadcast
+    const uint32_t upA = __shfl_up_sync(0xffffffffu, A, 1);
+    const uint32_t upB = __shfl_up_sync(0xffffffffu, B, 1);
+    const uint32_t a31 = __shfl_sync(0xffffffffu, A, 31);
+    A = (lane == 0 ? 0u : upA) ^ gf8_mul_log(g, lf, lgA);
+    B = (uint32_t)lane + 32 < TD ? ((lane == 0 ? a31 : upB) ^ gf8_mul_log(g, lf, lgB)) : 0u;
+  }
+  for (uint32_t j = lane; j < P::K; j += 32) cw[j] = msg[j];
+  if ((uint32_t)lane < TD) cw[P::N1 - 1 - lane] = (uint8_t)A;
+  if ((uint32_t)lane + 32 < TD) cw[P::N1 - 1 - (lane + 32)] = (uint8_t)B;
+}
+
 // The 128-bit RM(1,7) codeword of byte b (R#9): bit p = b7 ^ parity(b & 0x7F & p), word q = p >> 5.
 __device__ __forceinline__ void rm_encode_byte(uint32_t b, uint32_t (&w)[4]) {
   const uint32_t rows[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
@@ -287,11 +351,14 @@ template <class P> struct Enc2Smem {
   static_assert((P::E_STRIDE * 4) % 16 == 0, "support rows are TMA bulk copies");
   static constexpr uint32_t D_BYTES = round_up(round_up(P::WR, 4) * 4, 16);
   static constexpr uint32_t MISC_BYTES = round_up(P::N1 + P::K + 16, 16);
-  // two buffers of (r2 row, r1 or e row), prefetched by TMA one ciphertext ahead; two mbarriers
+  // two buffers of (r2 row, r1 or e row), prefetched by TMA one ciphertext ahead; two mbarriers. The
+  // rotation amounts of r2 are written over the r2 row (elementwise, in place): no separate array.
+  static_assert(D_BYTES <= SUP_BYTES, "the rotation amounts fit the r2 row");
   static constexpr uint32_t SUPS_BYTES = 4 * SUP_BYTES + 16;
-  static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + SUPS_BYTES + D_BYTES;
-  static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + SUPS_BYTES + D_BYTES + MISC_BYTES;
-  static constexpr uint32_t BYTES = W0_BYTES + W1_BYTES;
+  static constexpr uint32_t GF8_BYTES = sizeof(Gf8Tables);  // the encoder's log/antilog (warp 1), per CTA
+  static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + SUPS_BYTES;
+  static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + SUPS_BYTES + MISC_BYTES;
+  static constexpr uint32_t BYTES = GF8_BYTES + W0_BYTES + W1_BYTES;
 };
 
 #ifndef HQC_ENC2_MINB
@@ -309,13 +376,13 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
   extern __shared__ __align__(16) uint8_t smem[];
   using M = Enc2Smem<P>;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint8_t *base = smem + (wid ? M::W0_BYTES : 0u);
+  Gf8Tables *gf8 = reinterpret_cast<Gf8Tables *>(smem);
+  uint8_t *base = smem + M::GF8_BYTES + (wid ? M::W0_BYTES : 0u);
   uint32_t *E = reinterpret_cast<uint32_t *>(base);
   uint32_t *out = reinterpret_cast<uint32_t *>(base + (wid ? M::EV_BYTES : M::EU_BYTES));
   uint32_t *sups = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(out) + M::OUT_BYTES);
   uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sups) + 4 * M::SUP_BYTES);
-  uint32_t *dsm = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(sups) + M::SUPS_BYTES);
-  uint8_t *cw = reinterpret_cast<uint8_t *>(dsm) + M::D_BYTES;  // warp 1 only
+  uint8_t *cw = reinterpret_cast<uint8_t *>(sups) + M::SUPS_BYTES;  // warp 1 only
   uint8_t *msg = cw + P::N1;
   const size_t lo = (size_t)blockIdx.x * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
@@ -341,7 +408,9 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
   }
-  __syncwarp();
+  for (uint32_t i = threadIdx.x; i < sizeof(Gf8Tables) / 16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(gf8)[i] = __ldg(reinterpret_cast<const uint4 *>(&g_gf8) + i);
+  __syncthreads();
   uint32_t ph0 = 0, ph1 = 0;
   uint32_t mnext = (wid && lo < hi && (uint32_t)lane < P::K) ? m[lo * P::K + lane] : 0u;
   if (lo < hi) prefetch(lo, 0);
@@ -365,8 +434,9 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
     if (b) ph1 ^= 1u; else ph0 ^= 1u;
     __syncwarp();  // every lane has seen the rows land (and is done with buffer b ^ 1 of ciphertext ct - 1)
     if (ct + 1 < hi) prefetch(ct + 1, b ^ 1);
-    const uint32_t *s_r2 = sup_r2(b);
+    uint32_t *s_r2 = sup_r2(b);
     uint32_t *s_x = sup_x(b);
+    uint32_t *dsm = s_r2;  // the rotation amounts replace the r2 row entry by entry
     __syncwarp();
     uint32_t diff = 0;
     if (wid == 0) {  // u = r1 + h * r2 (all n bits)
@@ -401,7 +471,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       }
     } else {  // v = trunc(mG + s * r2 + e)
       using S = typename M::SV;
-      rs_encode_warp<P>(msg, cw, lane);
+      rs_encode_warp_log<P>(msg, cw, gf8, lane);
       s1_stage_d<P, S>(s_r2, dsm, lane);
       __syncwarp();
       uint32_t acc[S::R];
