@@ -12,7 +12,19 @@ __device__ unsigned long long g_phase_cycles[16];
     if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _t));     \
     _t = _n;                                                                                       \
   } while (0)
+// per-warp start / end times (%globaltimer, ns) of k_decrypt_sb, indexed by global warp id
+__device__ unsigned long long g_warp_span[8192][2];
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define WARP_SPAN(i, w)                                                      \
+  do {                                                                       \
+    if ((threadIdx.x & 31) == 0 && (w) < 8192) g_warp_span[(w)][(i)] = gtimer_ns(); \
+  } while (0)
 #else
 #define PHASE_T0()
 #define PHASE(i)
+#define WARP_SPAN(i, w)
 #endif

@@ -26,6 +26,11 @@ namespace hqc {
 #ifdef HQC_EXP_TIMING  // experiments only: per-phase cycle counters (exp_timing.cuh)
 #define HQC_CAT2(a, b) a##b
 #define HQC_CAT(a, b) HQC_CAT2(a, b)
+extern "C" int HQC_CAT(hqc_exp_warp_span_l, HQC_THIS_LEVEL)(unsigned long long *host, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, g_warp_span, sizeof(unsigned long long) * 2 * (n < 8192 ? n : 8192)) ==
+                 cudaSuccess ? 0 : -5;
+}
 extern "C" int HQC_CAT(hqc_exp_phases_l, HQC_THIS_LEVEL)(unsigned long long *host8) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(host8, g_phase_cycles, sizeof(unsigned long long) * 16);
@@ -388,7 +393,8 @@ template <class P> struct SbSmem {
   static constexpr uint32_t SYM_BYTES = round_up(P::N1, 16);  // the warp's received symbols
   static_assert(RsWarpScratch<P>::BYTES <= WarpSmem<P>::E_BYTES, "the RS scratch reuses the warp's E");
   static constexpr uint32_t WARP_BYTES = WarpSmem<P>::S1_BYTES + SYM_BYTES;
-  static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + g * WARP_BYTES; }
+  static constexpr uint32_t CTR_BYTES = 16;  // the CTA's work counter
+  static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + CTR_BYTES + g * WARP_BYTES; }
 };
 
 template <class P>
@@ -400,20 +406,33 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
   using M = SbSmem<P>;
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem + GF_BYTES);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t *ws = smem + GF_BYTES + (size_t)wib * M::WARP_BYTES;
+  const uint32_t G = blockDim.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + M::CTR_BYTES + (size_t)wib * M::WARP_BYTES;
   uint8_t *sym = ws + WarpSmem<P>::S1_BYTES;
   PHASE_T0();
   S1Pipe<P> pipe(ws, u, v, y, lane);
-  const size_t step = (size_t)gridDim.x * (blockDim.x >> 5);
-  size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (ct < batch) pipe.issue_uy(ct, lane);  // the first rows are in flight while the GF tables are copied
+  // The CTA owns the contiguous range [c0, c1); its warps take ciphertexts from it one at a time through a
+  // shared-memory counter (claimed one ciphertext ahead, so that its rows are prefetched during the current
+  // product). Statically strided warps ended up to 11% apart (HQC-3, 65,536: profiles/r02/warp_span.log):
+  // warps sharing an SM progress at different rates.
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  WARP_SPAN(0, (size_t)blockIdx.x * G + wib);
+  if (ct < c1) pipe.issue_uy(ct, lane);  // the first rows are in flight while the GF tables are copied
+  if (threadIdx.x == 0) *next_item = G;
   gf_tables_to_smem(gf);
   __syncthreads();
   if (stagger_ns) __nanosleep(stagger_ns * (uint32_t)wib);  // experiments: de-phase the warps of a CTA
   PHASE(0);
-  for (; ct < batch; ct += step) {
-    pipe.run(ct, ct + step < batch, ct + step, lane);
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    pipe.run(ct, nct < c1, nct, lane);
     PHASE_T0();
     for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in E)
       const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
@@ -430,7 +449,9 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
     rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(pipe.E), lane, m_out + ct * P::K);
     __syncwarp();  // E and sym are free for the next ciphertext
     PHASE(7);
+    ct = nct;
   }
+  WARP_SPAN(1, (size_t)blockIdx.x * G + wib);
 }
 
 

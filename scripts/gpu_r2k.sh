@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "small_batch or striding or decrypt_valid or adversarial_quarters or edges or full_size_config" > gpurun_out/pytest_dyn.log 2>&1; echo "exit $?" >> gpurun_out/pytest_dyn.log
+timeout 300 python scripts/exp_warp_span.py > gpurun_out/warp_span2.log 2>&1
+timeout 600 python scripts/exp_lib_ab.py paper_2512_12904_b200/libhqcgpu.so paper_2512_12904_b200/libhqcgpu.so 1:1024,3:1024,3:16384,3:65536,3:262144,1:16384,5:4096 > gpurun_out/ab_dyn.log 2>&1
