@@ -171,3 +171,24 @@ def test_kem_round_trip_with_seeded_keys(level):
     u, v, K = oracle.kem_encaps(p, h, s, hpk, m)
     K2, ok = oracle.kem_decaps(p, h, s, hpk, y, sigma, u, v)
     assert ok and K2 == K
+
+
+@pytest.mark.parametrize("n,w", [(5, 2), (6, 3), (7, 3), (8, 4)])
+def test_sampler_is_uniform_over_subsets(n, w):
+    """R#22's fixed-weight sampler pinned by what it must achieve, not by its formula: over EVERY tuple of
+    reduced draws o_i in [0, n-i) (rand_i chosen as the smallest 32-bit word with floor(rand_i (n-i) / 2^32)
+    = o_i), the outputs are w distinct positions < n and each of the C(n, w) subsets appears exactly w!
+    times — a uniform draw of a w-subset (the property the paper's "fixed-weight sampling", P:60, P:145,
+    needs). A variant that fixes a collision against EARLIER entries produces duplicates and skewed counts."""
+    import itertools
+    import math
+    from collections import Counter
+
+    cnt = Counter()
+    for offs in itertools.product(*[range(n - i) for i in range(w)]):
+        rnd = b"".join(int(-(-o * 2**32 // (n - i))).to_bytes(4, "little") for i, o in enumerate(offs))
+        pos = oracle.sample_fixed_weight(rnd, n, w)
+        assert len(set(pos.tolist())) == w and int(pos.max()) < n
+        cnt[tuple(sorted(pos.tolist()))] += 1
+    assert len(cnt) == math.comb(n, w)
+    assert set(cnt.values()) == {math.factorial(w)}

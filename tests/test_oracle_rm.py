@@ -80,3 +80,24 @@ def test_transform_definition_small_cases():
     s = (1 - 2 * bits.astype(np.int64)).sum(axis=0)
     F = oracle.rm_transform(blk, 3).astype(np.int64)
     assert (F ** 2).sum() == 128 * (s ** 2).sum()
+
+
+@pytest.mark.parametrize("level", [1, 3, 5])
+def test_code_encode_block_layout(level):
+    """R#12 pinned without the oracle's decoder: in code_encode(m), block j (bits
+    [j n2, (j+1) n2)) consists of mult identical 128-bit copies, and that copy is the codeword of RS symbol
+    j in the codebook above (whose parameters are pinned by Table I) — so symbol j lands in block j, in
+    order, copy c at +128c; and the RS symbols are rs_encode(m), message first (R#6)."""
+    p = oracle.params(level)
+    cb = np.stack([words_to_bits(oracle.rm_encode(b, 1), 128) for b in range(256)])
+    rng = np.random.default_rng(700 + level)
+    for _ in range(3):
+        m = rng.integers(0, 256, p.k).astype(np.uint8)
+        cw = oracle.rs_encode(m, p.n1, p.k)
+        assert (cw[: p.k] == m).all()
+        bits = words_to_bits(oracle.code_encode(p, m), p.n1 * p.n2)
+        for j in range(p.n1):
+            blk = bits[j * p.n2:(j + 1) * p.n2].reshape(p.mult, 128)
+            assert (blk == blk[0]).all(), f"copies of block {j} differ"
+            match = np.nonzero((cb == blk[0]).all(axis=1))[0]
+            assert match.tolist() == [int(cw[j])], f"block {j} is not the codeword of RS symbol {j}"
