@@ -66,6 +66,14 @@ template <class P> struct WarpSmem {
   static constexpr uint32_t BYTES = S1_BYTES + SYM_BYTES + R2_BYTES;               // fused kernel
 };
 
+// The one-warp products of S1Pipe with shifted lane windows (stage1.cuh: one SHFL.UP instead of the
+// (R+1)-th LDS per index and lane). Measured SLOWER (profiles/r02/ab_shfl.log: standalone product -1.5..-3%,
+// fused -0.6..-2.5%): the shuffle is served by the same shared-memory data path it was meant to spare.
+// Off; kept as an experiment switch.
+#ifndef HQC_S1_SHFL
+#define HQC_S1_SHFL 0
+#endif
+
 // Per-warp stage-1 pipeline: rows of ciphertext i+1 are fetched by TMA while ciphertext i is
 // computed (u and y during stage 2/3 of ciphertext i, v during its product loop).
 template <class P> struct S1Pipe {
@@ -114,8 +122,14 @@ template <class P> struct S1Pipe {
     wait();
     PHASE(1);
     using S = DecShape<P>;    // E and the staged rows
+#if HQC_S1_SHFL
+    using ST = DecShapeSh<P>;  // shifted lane windows (s1_product_range_sh); words [ST::NOUT, NW) by the tail
+    constexpr uint32_t TW = ST::TW;
+    static_assert(ST::E_WORDS <= S::E_WORDS, "the shifted windows stay inside E");
+#else
     using ST = DecShapeT<P>;  // the lanes' product; words [ST::NOUT, NW) by s1_tail_words
     constexpr uint32_t TW = dec_tail_words<P>();
+#endif
     s1_stage_d<P, S>(stg_y, dsm, lane);
     s1_build_E<P, S>(stg_u, E, lane);
     __syncwarp();
@@ -123,7 +137,11 @@ template <class P> struct S1Pipe {
     if (v) issue_v(ct, lane);
     else if (has_next) issue_uy(next, lane);  // no v to stage: the next rows land during this product
     uint32_t acc[ST::R];
+#if HQC_S1_SHFL
+    s1_product_range_sh<P, ST>(E, dsm, acc, lane, 0, P::W);
+#else
     s1_product<P, ST>(E, dsm, acc, lane);
+#endif
     uint32_t mine = 0;  // lane i < TW: word ST::NOUT + i
     if constexpr (TW > 0) {
       uint32_t t[TW];
@@ -135,10 +153,18 @@ template <class P> struct S1Pipe {
     PHASE(3);
     if (v) {
       wait();  // v has landed in the staging buffer during the product loop
+#if HQC_S1_SHFL
+      s1_store_r_xor_sh<ST>(acc, rout, stg_u, lane);
+#else
       s1_store_r_xor<ST>(acc, rout, stg_u, lane);
+#endif
       if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine ^ stg_u[ST::NOUT + lane];
     } else {
+#if HQC_S1_SHFL
+      s1_store_r_sh<ST>(acc, rout, lane);
+#else
       s1_store_r<ST>(acc, rout, lane);
+#endif
       if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine;
     }
     __syncwarp();

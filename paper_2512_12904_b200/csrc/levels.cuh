@@ -64,6 +64,24 @@ template <class P> constexpr uint32_t dec_tail_words() {
   return (HQC_S1_TAILW && P::NW - 32 * r > 0 && P::NW - 32 * r <= 8) ? P::NW - 32 * r : 0u;
 }
 template <class P> using DecShapeT = ProdShape<P, P::NW - dec_tail_words<P>(), P::W>;
+// The "shifted" lane windows of s1_product_range_sh (stage1.cuh): lane L owns the R output words
+// [L R - 1, L R + R - 1) (lane 0 one fewer), 32 R - 1 per warp; R odd. R is the largest odd value whose
+// 32 R - 1 words leave a ragged top of at most 9 words for s1_tail_words, else the smallest odd R that
+// covers all NW words.
+template <class P, uint32_t NW_, uint32_t WT_> struct ShShape {
+  static constexpr uint32_t NW = NW_, WT = WT_;
+  static constexpr uint32_t RLO = (((NW + 1) / 32) & 1u) ? (NW + 1) / 32 : (NW + 1) / 32 - 1;
+  static constexpr uint32_t RHI = make_odd_up((NW + 1 + 31) / 32);
+  static constexpr bool TAILED = (32 * RLO - 1 <= NW) && (NW - (32 * RLO - 1) <= 9);
+  static constexpr uint32_t R = TAILED ? RLO : RHI;
+  static constexpr uint32_t NOUT = TAILED ? 32 * R - 1 : NW;  // words the lanes produce (< 32 R)
+  static constexpr uint32_t TW = TAILED ? NW - NOUT : 0u;     // the ragged top (s1_tail_words)
+  static constexpr uint32_t E_WORDS = round_up(P::Q0 + 32 * R + 2 > 2 * P::Q0 + 2 ? P::Q0 + 32 * R + 2
+                                                                                  : 2 * P::Q0 + 2, 4);
+  static constexpr uint32_t WPAD = round_up(WT, 4);
+};
+template <class P> using DecShapeSh = ShShape<P, P::NW, P::W>;
+
 template <class P> using FullShape = ProdShape<P, P::Q0 + 1, P::WR>;    // h*r2: all n bits
 template <class P> using KeyShape = ProdShape<P, P::Q0 + 1, P::W>;      // h*y: all n bits
 template <class P> using EncVShape = ProdShape<P, P::NW, P::WR>;        // s*r2 truncated

@@ -178,6 +178,68 @@ __device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32
   }
 }
 
+// The same product with SHIFTED lane windows (ShShape, levels.cuh): lane L loads only the R words
+// E[o + L R + k], k < R, and takes the word before them, E[o + L R - 1] — the last word its left neighbour
+// loaded — with one SHFL.UP instead of an (R+1)-th shared-memory load: R loads per (index, lane) instead of
+// R + 1, i.e. 1/R fewer shared-memory wavefronts in the loop that binds every kernel.
+// acc[k] accumulates output word L R - 1 + k; lane 0's acc[0] (word -1) is garbage and never stored.
+template <class P, class S>
+__device__ __forceinline__ void s1_product_range_sh(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
+                                                    int lane, uint32_t j0, uint32_t j1) {
+  constexpr int R = S::R;
+#pragma unroll
+  for (int k = 0; k < R; k++) acc[k] = 0;
+  const uint32_t *Eb = E + lane * R;
+  uint32_t j = j0;
+  constexpr int kUnroll = s1_unroll<P>();
+#pragma unroll kUnroll
+  for (; j + 1 < j1; j += 2) {
+    const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
+    const uint32_t *p0 = s1_window<P>(Eb, dd.x);
+    const uint32_t *p1 = s1_window<P>(Eb, dd.y);
+    const uint32_t l0 = p0[R - 1], l1 = p1[R - 1];  // the last words first: the right neighbour needs them
+    uint32_t a0 = __shfl_up_sync(0xffffffffu, l0, 1), b0 = __shfl_up_sync(0xffffffffu, l1, 1);
+#pragma unroll
+    for (int k = 0; k < R; k++) {
+      const uint32_t a1 = k + 1 < R ? p0[k] : l0, b1 = k + 1 < R ? p1[k] : l1;
+      acc[k] ^= __funnelshift_r(a0, a1, dd.x) ^ __funnelshift_r(b0, b1, dd.y);
+      a0 = a1;
+      b0 = b1;
+    }
+  }
+  if (j < j1) {
+    const uint32_t d = dsm[j];
+    const uint32_t *p0 = s1_window<P>(Eb, d);
+    const uint32_t l0 = p0[R - 1];
+    uint32_t a0 = __shfl_up_sync(0xffffffffu, l0, 1);
+#pragma unroll
+    for (int k = 0; k < R; k++) {
+      const uint32_t a1 = k + 1 < R ? p0[k] : l0;
+      acc[k] ^= __funnelshift_r(a0, a1, d);
+      a0 = a1;
+    }
+  }
+}
+
+// Stores of the shifted accumulators: word L R - 1 + k (skipping lane 0's word -1), < S::NOUT.
+template <class S>
+__device__ __forceinline__ void s1_store_r_sh(const uint32_t (&acc)[S::R], uint32_t *rsm, int lane) {
+#pragma unroll
+  for (int k = 0; k < (int)S::R; k++) {
+    const int w = lane * (int)S::R - 1 + k;
+    if (w >= 0 && w < (int)S::NOUT) rsm[w] = acc[k];
+  }
+}
+template <class S>
+__device__ __forceinline__ void s1_store_r_xor_sh(const uint32_t (&acc)[S::R], uint32_t *rsm, const uint32_t *sv,
+                                                  int lane) {
+#pragma unroll
+  for (int k = 0; k < (int)S::R; k++) {
+    const int w = lane * (int)S::R - 1 + k;
+    if (w >= 0 && w < (int)S::NOUT) rsm[w] = acc[k] ^ sv[w];
+  }
+}
+
 template <class P, class S>
 __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
                                            int lane) {

@@ -448,6 +448,16 @@ def test_tensor_memory_variants_at_scale(tmp_path):
     hqc.hqc_decrypt_batch(1, to_dev(u), to_dev(v), to_dev(y), m)
     torch.cuda.synchronize()
     arrs.update({"du": u, "dv": v, "dy": y, "dm": m.cpu().numpy()})
+    # the reference outputs themselves against the oracle on sampled rows, so that the variants' equality
+    # below is a comparison with the oracle on those rows, not only with the default kernels
+    idx = np.random.default_rng(5).choice(B, 96, replace=False)
+    assert (arrs["dm"].reshape(B, hp.k)[idx] == oracle.decrypt_batch(p, u[idx], v[idx], y[idx])).all()
+    for level in (1, 3, 5):
+        op, hp_ = oracle.params(level), hqc.params(level)
+        Bl = arrs[f"u{level}"].shape[0]
+        ii = np.random.default_rng(level).choice(Bl, 48, replace=False)
+        ref = oracle.stage1_batch(op, arrs[f"u{level}"][ii], arrs[f"v{level}"][ii], arrs[f"y{level}"][ii])
+        assert (arrs[f"r{level}"].view(np.uint64).reshape(Bl, hp_.v_words)[ii] == ref).all()
     f = tmp_path / "ref.npz"
     np.savez(f, **arrs)
     code = r'''
