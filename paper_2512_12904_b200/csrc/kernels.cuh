@@ -414,11 +414,127 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
 // coefficients; no constant-bank tables, no CTA barrier). A CTA packs G such warps to share one copy of the
 // GF tables; the host picks G so that the batch spreads over all SMs (G = ceil(batch / SMs), capped by
 // shared memory), and warps stride over the batch when it is larger than the grid. Constant-flow.
+// The stage-1 pipe of k_decrypt_sb. Unlike S1Pipe, u lands by TMA DIRECTLY in the lower half of E
+// (E[q] = u32[q] for q < Q0: the copy out of a staging row is gone, only the shifted upper half is built),
+// r is formed in place over v in the staging buffer, and stages 2 and 3 work there (stage 3's scratch
+// too), so E is free once the product has read it: the next ciphertext's u is fetched into E during this
+// one's stages 2 and 3. Two mbarriers: u, y (bar[0]) and v (bar[1]) are in flight at the same time.
+template <class P> struct SbPipeSmem {
+  using S = DecShape<P>;
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static_assert(UB <= S::E_WORDS * 4, "u lands inside E");
+  static constexpr uint32_t E_BYTES = round_up(S::E_WORDS * 4, 16);
+  static constexpr uint32_t STG_BYTES = round_up(VB > RsWarpScratch<P>::BYTES ? VB : RsWarpScratch<P>::BYTES, 16);
+  static constexpr uint32_t Y_BYTES = round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t BYTES = E_BYTES + STG_BYTES + Y_BYTES + D_BYTES + 16;
+};
+
+template <class P> struct SbPipe {
+  using M = SbPipeSmem<P>;
+  uint32_t *E, *stg, *stg_y, *dsm;
+  uint64_t *bar;  // [0]: u, y   [1]: v
+  uint32_t ph_uy = 0, ph_v = 0;
+  const uint64_t *u, *v;
+  const uint32_t *y;
+
+  __device__ __forceinline__ SbPipe(uint8_t *ws, const uint64_t *u_, const uint64_t *v_, const uint32_t *y_, int lane)
+      : u(u_), v(v_), y(y_) {
+    E = reinterpret_cast<uint32_t *>(ws);
+    stg = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
+    stg_y = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::STG_BYTES);
+    dsm = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::STG_BYTES + M::Y_BYTES);
+    bar = reinterpret_cast<uint64_t *>(ws + M::E_BYTES + M::STG_BYTES + M::Y_BYTES + M::D_BYTES);
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void issue_uy(size_t ct, int lane) {  // E and stg_y must be free
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, M::UB + M::YB);
+      tma_load_1d(E, u + ct * P::U_STRIDE, M::UB, bar);
+      tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar);
+    }
+  }
+  // E from the u row already in its lower half: the shifted copy above word Q0 (E[Q0 + 1 + x] =
+  // funnel(u32[x], u32[x + 1], 32 - C), u32[Q0] masked to its C valid bits, u32[Q0 + 1] = 0), then word Q0
+  // itself (the wrap of X^n = 1) and the zero tail. Reads stay below word Q0, writes above it (lane 0 reads
+  // and rewrites word Q0 last), so no in-place hazard.
+  __device__ __forceinline__ void build_E(int lane) {
+    using S = DecShape<P>;
+    constexpr uint32_t MASK_C = (1u << P::C) - 1u;
+    constexpr uint32_t NF = P::Q0 - 1;                  // x = 0 .. Q0 - 2: both sources below word Q0
+    constexpr uint32_t CH = ((NF + 31) / 32) | 1u;      // per-lane run, odd: conflict-free
+    uint32_t eq0 = 0, s0 = 0, sl = 0;
+    if (lane == 0) {
+      eq0 = E[P::Q0] & MASK_C;
+      s0 = E[0];
+      sl = E[P::Q0 - 1];
+    }
+    const uint32_t x0 = (uint32_t)lane * CH;
+    uint32_t lo = x0 < NF ? E[x0] : 0u;
+#pragma unroll 4
+    for (uint32_t t = 0; t < CH; t++) {
+      const uint32_t x = x0 + t;
+      if (x < NF) {
+        const uint32_t hi = E[x + 1];
+        E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+        lo = hi;
+      }
+    }
+    if (lane == 0) {
+      E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);      // x = Q0 - 1
+      E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);  // x = Q0
+      E[P::Q0] = eq0 | (s0 << P::C);
+    }
+    for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
+  }
+  // Stage 1 of ct (its u, y requested); leaves r in stg; requests next's u, y as soon as E is read.
+  __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
+    using S = DecShape<P>;
+    using ST = DecShapeT<P>;
+    constexpr uint32_t TW = dec_tail_words<P>();
+    PHASE_T0();
+    mbar_wait(bar, ph_uy);
+    ph_uy ^= 1u;
+    PHASE(1);
+    s1_stage_d<P, S>(stg_y, dsm, lane);
+    build_E(lane);
+    __syncwarp();
+    PHASE(2);
+    if (lane == 0) {  // v lands in stg during the product
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar + 1, M::VB);
+      tma_load_1d(stg, v + ct * P::V_WORDS, M::VB, bar + 1);
+    }
+    uint32_t acc[ST::R];
+    s1_product<P, ST>(E, dsm, acc, lane);
+    uint32_t mine = 0;  // lane i < TW: word ST::NOUT + i
+    if constexpr (TW > 0) {
+      uint32_t t[TW];
+      s1_tail_words<P, ST, ST::NOUT, TW>(E, dsm, lane, t);
+#pragma unroll
+      for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
+    }
+    __syncwarp();  // every lane is done reading E (and dsm, stg_y): the next rows may land
+    PHASE(3);
+    if (has_next) issue_uy(next, lane);
+    mbar_wait(bar + 1, ph_v);
+    ph_v ^= 1u;
+    s1_store_r_xor<ST>(acc, stg, stg, lane);  // r = acc ^ v, word by word in place (each lane its own words)
+    if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine ^ stg[ST::NOUT + lane];
+    __syncwarp();
+    PHASE(4);
+  }
+};
+
 template <class P> struct SbSmem {
   static constexpr uint32_t MAX_G = 16;  // warps per CTA; 512 threads: <= 128 registers
   static constexpr uint32_t SYM_BYTES = round_up(P::N1, 16);  // the warp's received symbols
-  static_assert(RsWarpScratch<P>::BYTES <= WarpSmem<P>::E_BYTES, "the RS scratch reuses the warp's E");
-  static constexpr uint32_t WARP_BYTES = WarpSmem<P>::S1_BYTES + SYM_BYTES;
+  static constexpr uint32_t WARP_BYTES = SbPipeSmem<P>::BYTES + SYM_BYTES;
   static constexpr uint32_t CTR_BYTES = 16;  // the CTA's work counter
   static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + CTR_BYTES + g * WARP_BYTES; }
 };
@@ -436,9 +552,9 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t G = blockDim.x >> 5;
   uint8_t *ws = smem + GF_BYTES + M::CTR_BYTES + (size_t)wib * M::WARP_BYTES;
-  uint8_t *sym = ws + WarpSmem<P>::S1_BYTES;
+  uint8_t *sym = ws + SbPipeSmem<P>::BYTES;
   PHASE_T0();
-  S1Pipe<P> pipe(ws, u, v, y, lane);
+  SbPipe<P> pipe(ws, u, v, y, lane);
   // The CTA owns the contiguous range [c0, c1); its warps take ciphertexts from it one at a time through a
   // shared-memory counter (claimed one ciphertext ahead, so that its rows are prefetched during the current
   // product). Statically strided warps ended up to 11% apart (HQC-3, 65,536: profiles/r02/warp_span.log):
@@ -460,8 +576,8 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
     const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
     pipe.run(ct, nct < c1, nct, lane);
     PHASE_T0();
-    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in E)
-      const uint4 *src = reinterpret_cast<const uint4 *>(pipe.E) + j * (P::N2 / 128);
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in the staging buffer)
+      const uint4 *src = reinterpret_cast<const uint4 *>(pipe.stg) + j * (P::N2 / 128);
       uint32_t X[P::MULT * 4];
 #pragma unroll
       for (int c = 0; c < (int)P::MULT; c++) {
@@ -470,9 +586,9 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
       }
       sym[j] = (uint8_t)rm_decode_block<P::MULT>(X);
     }
-    __syncwarp();  // the symbols are complete and r (in E) is consumed
+    __syncwarp();  // the symbols are complete and r is consumed: the staging buffer is stage 3's scratch
     PHASE(5);
-    rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(pipe.E), lane, m_out + ct * P::K);
+    rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(pipe.stg), lane, m_out + ct * P::K);
     __syncwarp();  // E and sym are free for the next ciphertext
     PHASE(7);
     ct = nct;
