@@ -240,10 +240,59 @@ __device__ __forceinline__ void s1_store_r_xor_sh(const uint32_t (&acc)[S::R], u
   }
 }
 
+// All S::WT indices (from 0, so dsm is 16-byte aligned at every group of four): the rotation amounts of
+// four indices come in one broadcast 16-byte load (one shared-memory wavefront instead of two).
+// Measured (profiles/r02/ab_dd4.log): HQC-3 fused 1.160 -> 1.140 ms, HQC-1 standalone 0.354 -> 0.348 ms,
+// HQC-5 fused -0.35% (its unroll-3 pair loop stays).
+#ifndef HQC_S1_DD4
+#define HQC_S1_DD4 (P::level != 5)
+#endif
 template <class P, class S>
 __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
                                            int lane) {
-  s1_product_range<P, S>(E, dsm, acc, lane, 0, S::WT);
+  if constexpr (!HQC_S1_DD4) {
+    s1_product_range<P, S>(E, dsm, acc, lane, 0, S::WT);
+  } else {
+    constexpr int R = S::R;
+#pragma unroll
+    for (int k = 0; k < R; k++) acc[k] = 0;
+    const uint32_t *Eb = E + lane * R;
+    auto pair = [&](uint32_t dx, uint32_t dy) {
+      const uint32_t *p0 = s1_window<P>(Eb, dx);
+      const uint32_t *p1 = s1_window<P>(Eb, dy);
+      uint32_t a0 = p0[0], b0 = p1[0];
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        const uint32_t a1 = p0[k + 1], b1 = p1[k + 1];
+        acc[k] ^= __funnelshift_r(a0, a1, dx) ^ __funnelshift_r(b0, b1, dy);
+        a0 = a1;
+        b0 = b1;
+      }
+    };
+    uint32_t j = 0;
+#pragma unroll 1
+    for (; j + 3 < S::WT; j += 4) {
+      const uint4 d4 = *reinterpret_cast<const uint4 *>(dsm + j);
+      pair(d4.x, d4.y);
+      pair(d4.z, d4.w);
+    }
+    if constexpr (S::WT % 4 >= 2) {
+      const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
+      pair(dd.x, dd.y);
+      j += 2;
+    }
+    if constexpr (S::WT % 2) {
+      const uint32_t d = dsm[j];
+      const uint32_t *p0 = s1_window<P>(Eb, d);
+      uint32_t a0 = p0[0];
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        const uint32_t a1 = p0[k + 1];
+        acc[k] ^= __funnelshift_r(a0, a1, d);
+        a0 = a1;
+      }
+    }
+  }
 }
 
 // Words [Q, Q + TW) of the product by the whole warp (the ragged top above the lanes' R-word blocks): lane
