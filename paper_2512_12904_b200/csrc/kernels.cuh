@@ -1059,12 +1059,13 @@ static long env_long(const char *name, long dflt) {
   const char *s = getenv(name);
   return s && *s ? atol(s) : dflt;
 }
-// K4s up to this batch (scripts/sweep_launch.py small / large, profiles/r02/sweep_*.log):
-// HQC-3 at every batch (65,536: 5.61e7/s vs 5.41e7 for the warp pair K4; 262,144: 5.79e7 vs 5.53e7);
-// HQC-1 up to 32,768 (1.02e8 vs 9.18e7; at 65,536 K4a's paired RM stage and lane-per-word RS win,
-// 1.19e8 vs 1.05e8); HQC-5 up to 8,192 (its shared memory allows 10 warps per SM in K4s, 16 in K4a).
+// K4s up to this batch (scripts/sweep_launch.py small / large / cross, profiles/r02/
+// sweep_*.log): HQC-3 at every batch (65,536: 5.61e7/s vs 5.41e7 for the warp pair K4; 262,144: 5.79e7 vs
+// 5.53e7); HQC-1 up to ~40,000 (32,768: 1.04e8 vs 9.28e7; 49,152: 1.06e8 vs 1.10e8 — beyond, K4a's paired
+// RM stage and lane-per-word RS win); HQC-5 up to ~24,000 (16,384: 2.41e7 vs 2.24e7; 32,768: 2.37e7 vs
+// 2.58e7 — its shared memory allows 10 warps per SM in K4s, 8 in K4a but with the cheaper lane RS).
 template <class P> static size_t sb_max_batch(int sms) {
-  const long dflt = P::level == 3 ? -1L : (long)sms * (P::level == 1 ? 224 : 56);
+  const long dflt = P::level == 3 ? -1L : (long)sms * (P::level == 1 ? 270 : 160);
   const long v = env_long("HQC_SB_MAX", dflt);
   return v < 0 ? ~(size_t)0 : (size_t)v;
 }
