@@ -178,27 +178,31 @@ constexpr uint32_t GF_BYTES = round_up(sizeof(GfTables), 16);
 constexpr int WARPS_PER_CTA_S1 = 1;  // stage-1 kernel CTA size (warps)
 
 // ------------------------------------------------------------------------------------------------
-// K1: stage 1 alone. One warp per ciphertext (grid-stride over warps).
+// K1: stage 1 alone. One warp per ciphertext (grid-stride over warps), on the pipe of k_decrypt_sb
+// (SbPipe, defined with it below): u lands by TMA in E's lower half, r is formed in the staging buffer and
+// leaves by a TMA bulk store, and the next u is fetched into E as soon as the product has read it.
 #ifndef HQC_S1K_MINB
 #define HQC_S1K_MINB 1  // lets the compiler keep loads ahead (HQC-3 standalone product -4%)
 #endif
+template <class P> struct SbPipe;
+template <class P> struct SbPipeSmem;
 template <class P>
 __global__ void __launch_bounds__(32 * WARPS_PER_CTA_S1, HQC_S1K_MINB) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
                                                 const uint64_t *__restrict__ v, uint64_t *__restrict__ r_out,
                                                 size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  S1Pipe<P> pipe(smem + (size_t)wib * WarpSmem<P>::S1_BYTES, u, v, y, lane);
+  SbPipe<P> pipe(smem + (size_t)wib * SbPipeSmem<P>::BYTES, u, v, y, lane);
   const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
   size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (ct < batch) pipe.issue_uy(ct, lane);
   for (; ct < batch; ct += nwarps) {
-    if (lane == 0) tma_store_wait_read();  // the previous r (in E) has been read by its store
+    if (lane == 0) tma_store_wait_read();  // the previous r (in the staging buffer) has been read by its store
     __syncwarp();
     pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
-    fence_proxy_async_smem();  // r (in E) -> HBM by a TMA bulk store, asynchronous to the next product
+    fence_proxy_async_smem();  // r -> HBM by a TMA bulk store, asynchronous to the next product
     __syncwarp();
-    if (lane == 0) tma_store_1d(r_out + ct * P::V_WORDS, pipe.E, P::V_WORDS * 8);
+    if (lane == 0) tma_store_1d(r_out + ct * P::V_WORDS, pipe.stg, P::V_WORDS * 8);
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -505,7 +509,7 @@ template <class P> struct SbPipe {
     build_E(lane);
     __syncwarp();
     PHASE(2);
-    if (lane == 0) {  // v lands in stg during the product
+    if (v && lane == 0) {  // v lands in stg during the product
       fence_proxy_async_smem();
       mbar_expect_tx(bar + 1, M::VB);
       tma_load_1d(stg, v + ct * P::V_WORDS, M::VB, bar + 1);
@@ -522,10 +526,15 @@ template <class P> struct SbPipe {
     __syncwarp();  // every lane is done reading E (and dsm, stg_y): the next rows may land
     PHASE(3);
     if (has_next) issue_uy(next, lane);
-    mbar_wait(bar + 1, ph_v);
-    ph_v ^= 1u;
-    s1_store_r_xor<ST>(acc, stg, stg, lane);  // r = acc ^ v, word by word in place (each lane its own words)
-    if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine ^ stg[ST::NOUT + lane];
+    if (v) {
+      mbar_wait(bar + 1, ph_v);
+      ph_v ^= 1u;
+      s1_store_r_xor<ST>(acc, stg, stg, lane);  // r = acc ^ v, word by word in place (each lane its own words)
+      if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine ^ stg[ST::NOUT + lane];
+    } else {  // the standalone product: r = acc
+      s1_store_r<ST>(acc, stg, lane);
+      if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine;
+    }
     __syncwarp();
     PHASE(4);
   }
@@ -1093,7 +1102,7 @@ template <class P> static int stage1_kernel() {
   if (env == 1 || env == 2 || env == 3) return env;
   return P::level == 5 ? 2 : 1;
 }
-template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * WarpSmem<P>::S1_BYTES; }
+template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * SbPipeSmem<P>::BYTES; }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }

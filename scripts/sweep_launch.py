@@ -84,6 +84,9 @@ if __name__ == "__main__":
         small([1, 3, 5], [1, 8, 33, 148, 296, 512, 1024, 1184, 2048, 4096, 8192, 16384])
     elif what == "large":
         small([1, 3, 5], [32768, 65536, 262144])
+    elif what == "cross":
+        small([1], [16384, 32768, 49152, 65536, 131072])
+        small([5], [4096, 8192, 16384, 32768, 65536])
     elif what == "stagger":
         dev = torch.device("cuda:0")
         cases = [tuple(map(int, c.split(":"))) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
