@@ -410,6 +410,99 @@ __global__ void __launch_bounds__(32, HQC_DEC_MINCTAS_W1) k_decrypt_w1(const uin
 }
 
 
+// K4d: K4a (chunks of 32 decryptions per warp, paired RM stage for HQC-1, lane-per-word RS) with the
+// warps of a CTA sharing the work: the CTA owns a contiguous range and its G warps take decryptions from it
+// one at a time through a shared-memory counter (claimed one ahead for the TMA prefetch), each warp filling
+// its own chunk of symbol rows and decoding it when it holds 32 or the range runs out. K4a's one-warp CTAs
+// own fixed ranges, and on HQC-1 the SM averaged 13.1 active warps of the 15.8 resident
+// (profiles/r02/ncu_fused.md): warps sharing an SM progress at different rates and the early finishers idle.
+template <class P> struct WdSmem {
+  static constexpr uint32_t IDX_BYTES = 32 * 4;  // the chunk's decryption indices
+  static constexpr uint32_t WARP_BYTES = WarpSmem<P>::BYTES + IDX_BYTES;
+  static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + 16 + g * WARP_BYTES; }
+  // warps per CTA: at most 16 (512 threads, <= 128 registers), fewer where shared memory runs out
+  // (HQC-3: 13 of 16.4 KB, HQC-5: 8 of 26 KB)
+  static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
+  static constexpr uint32_t MAX_G = fit(16);
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * WdSmem<P>::MAX_G, 1) k_decrypt_wd(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out,
+                                                                        size_t batch) {
+  using M = WdSmem<P>;
+  using W = WarpSmem<P>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem + GF_BYTES);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t G = blockDim.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + 16 + (size_t)wib * M::WARP_BYTES;
+  S1Pipe<P> pipe(ws, u, v, y, lane);
+  uint8_t *sb = ws + W::S1_BYTES;
+  uint32_t *R2 = reinterpret_cast<uint32_t *>(sb + W::SYM_BYTES);
+  uint32_t *cidx = reinterpret_cast<uint32_t *>(ws + W::BYTES);
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) pipe.issue_uy(ct, lane);
+  if (threadIdx.x == 0) *next_item = G;
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  auto stage2 = [&](const uint32_t *r0, uint32_t s0, const uint32_t *r1, uint32_t s1, uint32_t nblk) {
+    for (uint32_t t = lane; t < nblk; t += 32) {
+      const bool second = t >= P::N1;
+      const uint32_t j = second ? t - P::N1 : t;
+      const uint4 *src = reinterpret_cast<const uint4 *>(second ? r1 : r0) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      sb[j * W::SYM_PITCH + (second ? s1 : s0)] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+  };
+  uint32_t s = 0;  // slot of ct in the warp's current chunk
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    const bool more = nct < c1;
+    if (lane == 0) cidx[s] = (uint32_t)(ct - c0);
+    if constexpr (W::PAIR_S2) {
+      if ((s & 1) == 0 && s + 1 < 32 && more) {  // park r in R2; decoded together with the next one
+        pipe.run(ct, true, nct, lane, R2);
+      } else {
+        pipe.run(ct, more, nct, lane);
+        if (s & 1) stage2(R2, s - 1, pipe.E, s, 2 * P::N1);
+        else stage2(pipe.E, s, pipe.E, s, P::N1);
+      }
+    } else {
+      pipe.run(ct, more, nct, lane);
+      stage2(pipe.E, s, pipe.E, s, P::N1);
+    }
+    __syncwarp();
+    s++;
+    if (s == 32 || !more) {  // the chunk is full, or this warp's last decryption: stage 3, lane per word
+      for (uint32_t q = s; q < 32; q++)
+        for (uint32_t j = lane; j < P::N1; j += 32) sb[j * W::SYM_PITCH + q] = 0;
+      __syncwarp();
+      const bool act = (uint32_t)lane < s;
+      auto sym_at = [&](int j) -> uint32_t { return sb[j * W::SYM_PITCH + lane]; };
+      rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(pipe.E), lane,
+                        act ? m_out + (c0 + cidx[lane]) * P::K : nullptr);
+      __syncwarp();
+      s = 0;
+    }
+    ct = nct;
+  }
+}
+
+
 // K4s: fused decrypt for SMALL batches (BASELINE configs[0]: HQC-1 at 1,024). K4a gives every warp at
 // least 16 consecutive ciphertexts, so a batch of 1,024 occupies 64 warps on 64 SMs and the launch is the
 // latency of 16 products in a row plus a lane-per-word RS decode. Here every warp takes ONE ciphertext at a
@@ -1049,18 +1142,21 @@ template <class P> static uint32_t decrypt_ws_smem() { return GF_BYTES + WsSmem<
 template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_BYTES; }
 
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
-// 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s).
-// HQC_DEC_KERNEL=1..5 overrides (experiments and tests).
+// 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
+// 6 = K4a with CTA-shared work (K4d). HQC_DEC_KERNEL=1..6 overrides (experiments and tests).
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 5 ? env : 0;
+  return env >= 1 && env <= 6 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
-  return P::level == 3 ? 2 : 1;  // occupancy sweeps: one warp wins for HQC-1 (0.629 vs 0.645 ms) and HQC-5
+  // above the K4s range: HQC-1 K4d (65,536: 0.526 vs 0.560 ms for K4a; 262,144: +6.7%,
+  // profiles/r02/ab_wd.log), HQC-5 K4a (K4d -3%: 8 warps per SM either way, and K4d's 239 registers per
+  // thread buy nothing there); HQC-3 never gets here (K4s at every batch)
+  return P::level == 1 ? 6 : P::level == 3 ? 2 : 1;
 }
 // Read on every call (experiments sweep them within one process): HQC_SB_MAX = the largest batch that
 // takes K4s by default; HQC_DEC_SPLIT = the most ciphertexts one launch of the large-batch kernels takes.
@@ -1124,6 +1220,8 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaFuncSetAttribute(k_decrypt_ws<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_ws<P>, 128, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt_ws[P::level] = c > 0 ? c : 1;
+  if ((e = cudaFuncSetAttribute(k_decrypt_wd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 SbSmem<P>::bytes(sb_max_g<P>()))) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
@@ -1153,6 +1251,15 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     const size_t cap = (size_t)di.sms * (227u * 1024u / SbSmem<P>::bytes((uint32_t)g) > 0
                                              ? 227u * 1024u / SbSmem<P>::bytes((uint32_t)g) : 1u);
     *grid = (int)(groups < cap ? groups : cap);
+    return;
+  }
+  if (kind == 6) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > WdSmem<P>::MAX_G) g = WdSmem<P>::MAX_G;
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
     return;
   }
   if (kind == 4) {  // one CTA of WARPS warps per SM; at least 16 ciphertexts per warp
@@ -1202,6 +1309,9 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
           cudaSuccess)
         return HQC_ERR_CUDA;
       k_decrypt_t<P><<<grid, 32 * TmDec<P>::WARPS, decrypt_t_smem<P>(), st>>>(u, v, y, m, batch, per);
+      break;
+    case 6:
+      k_decrypt_wd<P><<<grid, 32 * (unsigned)per, WdSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
       break;
     case 5:
       k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
@@ -1361,7 +1471,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
-  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : kind == 5 ? (int)per : 4;
+  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : (kind == 5 || kind == 6) ? (int)per : 4;
   return HQC_OK;
 }
 

@@ -28,8 +28,16 @@ for c in sys.argv[2].split(","):
 '''.replace("ROOT", ROOT)
 
 if __name__ == "__main__":
+    # an argument "KERNEL=k@LIB" runs LIB with HQC_DEC_KERNEL=k
     for rep in range(2):
         for lib in sys.argv[1:3]:
-            r = subprocess.run([sys.executable, "-c", CODE, lib, sys.argv[3]], capture_output=True, text=True, cwd=ROOT)
+            env = dict(os.environ)
+            if "@" in lib:
+                kv, lib = lib.split("@")
+                env["HQC_DEC_KERNEL"] = kv.split("=")[1]
+            r = subprocess.run([sys.executable, "-c", CODE, lib, sys.argv[3]], capture_output=True, text=True, cwd=ROOT,
+                               env=env)
+            if "HQC_DEC_KERNEL" in env:
+                sys.stdout.write(f"# HQC_DEC_KERNEL={env['HQC_DEC_KERNEL']}\n")
             sys.stdout.write(r.stdout + (r.stderr[-2000:] if r.returncode else ""))
             sys.stdout.flush()

@@ -104,4 +104,5 @@ if __name__ == "__main__":
             os.environ.pop("HQC_SB_STAGGER")
     elif what == "split":
         B = int(sys.argv[2]) if len(sys.argv) > 2 else 4_194_304
-        split([1, 3, 5], B, [0, 32768, 65536, 131072, 262144, 524288, 1048576])
+        levels = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 3, 5]
+        split(levels, B, [0, 32768, 65536, 131072, 262144, 524288, 1048576])
