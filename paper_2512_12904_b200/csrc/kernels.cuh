@@ -341,7 +341,9 @@ __global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym,
 #define HQC_DEC_MINCTAS (P::level == 5 ? 6 : (P::level == 1 ? 14 : 8))
 #endif
 #ifndef HQC_DEC_MINCTAS_W1
-#define HQC_DEC_MINCTAS_W1 (P::level == 5 ? 14 : (P::level == 1 ? 16 : 12))
+// (HQC-5: shared memory holds 8 one-warp CTAs per SM anyway; a cap of 14 forced 128 registers and spills,
+// 8 lets it keep 239: +0.2-0.3%, profiles/r02/ab_w1m.log)
+#define HQC_DEC_MINCTAS_W1 (P::level == 5 ? 8 : (P::level == 1 ? 16 : 12))
 #endif
 
 // K4a: fused decrypt, one warp per ciphertext (the pair-free variant). Warp g owns ciphertexts
