@@ -242,10 +242,10 @@ __device__ __forceinline__ void s1_store_r_xor_sh(const uint32_t (&acc)[S::R], u
 
 // All S::WT indices (from 0, so dsm is 16-byte aligned at every group of four): the rotation amounts of
 // four indices come in one broadcast 16-byte load (one shared-memory wavefront instead of two).
-// Measured (profiles/r02/ab_dd4.log): HQC-3 fused 1.160 -> 1.140 ms, HQC-1 standalone 0.354 -> 0.348 ms,
-// HQC-5 fused -0.35% (its unroll-3 pair loop stays).
+// Measured against the same build without it (profiles/r02/ab_dd4_clean.log): no difference within
+// ±0.4% (the 25-50 wavefronts it saves per decryption are not what limits), so off; an experiment switch.
 #ifndef HQC_S1_DD4
-#define HQC_S1_DD4 (P::level != 5)
+#define HQC_S1_DD4 0
 #endif
 template <class P, class S>
 __device__ __forceinline__ void s1_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
