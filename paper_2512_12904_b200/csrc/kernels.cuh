@@ -701,6 +701,151 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
 }
 
 
+// K4p: small batches with a warp PAIR per decryption (configs[0]: 1,024 decryptions are 7 per SM, and a
+// launch is the latency of one decryption: product ~10k cycles — the SM's shared memory saturated by its 7
+// products — stage 2 6.6k in two rounds of 32 lanes, stage 3 ~10.7k; profiles/r02/sb_phases*.log). The pair
+// shares E: warp A builds it from the u row TMA put in its lower half (the SbPipe layout), both run the
+// product over half of the support indices, B's accumulators meet A's and v in the staging buffer, and
+// stage 2 is split between the warps (one round each for n1 <= 64); warp A runs stage 3 (stage3_warp.cuh).
+// A named barrier per pair (ids 1..8) orders the steps; the pairs of a CTA share only the GF tables.
+template <class P> struct SpSmem {
+  using S = DecShape<P>;
+  using ST = DecShapeT<P>;
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t E_BYTES = round_up(S::E_WORDS * 4, 16);
+  static constexpr uint32_t STG_BYTES = round_up(VB > RsWarpScratch<P>::BYTES ? VB : RsWarpScratch<P>::BYTES, 16);
+  static constexpr uint32_t X_BYTES = round_up(P::NW * 4, 16);  // warp B's accumulator image
+  static constexpr uint32_t Y_BYTES = round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1, 16);
+  static constexpr uint32_t PAIR_BYTES = E_BYTES + STG_BYTES + X_BYTES + Y_BYTES + D_BYTES + SYM_BYTES + 16;
+  static constexpr uint32_t MAX_PAIRS = 8;  // named barriers 1..8; 512 threads
+  static constexpr uint32_t bytes(uint32_t pairs) { return GF_BYTES + pairs * PAIR_BYTES; }
+  static constexpr uint32_t W0 = (P::W / 2) & ~1u;  // warp A: indices [0, W0), warp B: [W0, W)
+};
+
+__device__ __forceinline__ void pair_sync(uint32_t id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+template <class P>
+__global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(const uint64_t *__restrict__ u,
+                                                                           const uint64_t *__restrict__ v,
+                                                                           const uint32_t *__restrict__ y,
+                                                                           uint8_t *__restrict__ m_out,
+                                                                           size_t batch) {
+  using M = SpSmem<P>;
+  using S = typename M::S;
+  using ST = typename M::ST;
+  constexpr uint32_t TW = dec_tail_words<P>();
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t pr = (uint32_t)wib >> 1, wa = (uint32_t)wib & 1u;  // pair, warp of the pair (0 = A)
+  const uint32_t npairs = blockDim.x >> 6;
+  uint8_t *ps = smem + GF_BYTES + (size_t)pr * M::PAIR_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(ps);
+  uint32_t *stg = reinterpret_cast<uint32_t *>(ps + M::E_BYTES);
+  uint32_t *X = reinterpret_cast<uint32_t *>(ps + M::E_BYTES + M::STG_BYTES);
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(ps + M::E_BYTES + M::STG_BYTES + M::X_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ps + M::E_BYTES + M::STG_BYTES + M::X_BYTES + M::Y_BYTES);
+  uint8_t *sym = ps + M::E_BYTES + M::STG_BYTES + M::X_BYTES + M::Y_BYTES + M::D_BYTES;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sym + M::SYM_BYTES);  // [0]: u, y   [1]: v
+  const uint32_t bid = 1 + pr;
+  if (wa == 0 && lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  const size_t step = (size_t)gridDim.x * npairs;
+  size_t ct = (size_t)blockIdx.x * npairs + pr;
+  auto issue_uy = [&](size_t c) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, M::UB + M::YB);
+    tma_load_1d(E, u + c * P::U_STRIDE, M::UB, bar);
+    tma_load_1d(stg_y, y + c * P::Y_STRIDE, M::YB, bar);
+  };
+  gf_tables_to_smem(gf);
+  __syncthreads();  // mbarriers initialised, GF tables in place
+  if (wa == 0 && lane == 0 && ct < batch) issue_uy(ct);
+  uint32_t ph_uy = 0, ph_v = 0;
+  for (; ct < batch; ct += step) {
+    const bool has_next = ct + step < batch;
+    if (wa == 0) {
+      mbar_wait(bar, ph_uy);
+      s1_stage_d<P, S>(stg_y, dsm, lane);
+      // E from the u row in its lower half (as SbPipe::build_E)
+      constexpr uint32_t MASK_C = (1u << P::C) - 1u;
+      constexpr uint32_t NF = P::Q0 - 1;
+      constexpr uint32_t CH = ((NF + 31) / 32) | 1u;
+      uint32_t eq0 = 0, s0 = 0, sl = 0;
+      if (lane == 0) {
+        eq0 = E[P::Q0] & MASK_C;
+        s0 = E[0];
+        sl = E[P::Q0 - 1];
+      }
+      const uint32_t x0 = (uint32_t)lane * CH;
+      uint32_t lo = x0 < NF ? E[x0] : 0u;
+#pragma unroll 4
+      for (uint32_t t = 0; t < CH; t++) {
+        const uint32_t x = x0 + t;
+        if (x < NF) {
+          const uint32_t hi = E[x + 1];
+          E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+          lo = hi;
+        }
+      }
+      if (lane == 0) {
+        E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);
+        E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);
+        E[P::Q0] = eq0 | (s0 << P::C);
+      }
+      for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
+      __syncwarp();
+      if (lane == 0) {  // v lands in stg during the product
+        fence_proxy_async_smem();
+        mbar_expect_tx(bar + 1, M::VB);
+        tma_load_1d(stg, v + ct * P::V_WORDS, M::VB, bar + 1);
+      }
+    }
+    ph_uy ^= 1u;
+    pair_sync(bid);  // E and the rotation amounts are ready
+    uint32_t acc[ST::R];
+    s1_product_range<P, ST>(E, dsm, acc, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
+    uint32_t mine = 0;
+    if constexpr (TW > 0) {
+      if (wa == 0) {
+        uint32_t t[TW];
+        s1_tail_words<P, ST, ST::NOUT, TW>(E, dsm, lane, t);
+#pragma unroll
+        for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
+      }
+    }
+    if (wa) s1_store_r<ST>(acc, X, lane);
+    pair_sync(bid);  // both warps are done with E; B's image is in X
+    if (wa == 0) {
+      if (has_next && lane == 0) issue_uy(ct + step);
+      mbar_wait(bar + 1, ph_v);
+      s1_store_r_xor2<ST>(acc, stg, X, stg, lane);  // r = acc_A ^ acc_B ^ v, in place over v
+      if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine ^ stg[ST::NOUT + lane];
+    }
+    ph_v ^= 1u;
+    pair_sync(bid);  // r complete
+    constexpr uint32_t NH = (P::N1 + 1) / 2;  // stage 2: A blocks [0, NH), B [NH, n1)
+    for (uint32_t j = (wa ? NH : 0u) + lane; j < (wa ? P::N1 : NH); j += 32) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(stg) + j * (P::N2 / 128);
+      uint32_t Xv[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        Xv[4 * c] = x.x; Xv[4 * c + 1] = x.y; Xv[4 * c + 2] = x.z; Xv[4 * c + 3] = x.w;
+      }
+      sym[j] = (uint8_t)rm_decode_block<P::MULT>(Xv);
+    }
+    pair_sync(bid);  // symbols complete, r consumed
+    if (wa == 0) rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(stg), lane, m_out + ct * P::K);
+    pair_sync(bid);  // stg and sym free for the next decryption
+  }
+}
+
+
 // K4t: fused decrypt with the product's windows in TENSOR MEMORY (stage1_tmem.cuh), one CTA per SM of
 // WARPS warps; warp g owns ciphertexts [g*per, (g+1)*per) in chunks of 32 like K4a: stage 1 (TmPipe) +
 // stage 2 per ciphertext (symbols parked as [j][slot]), then stage 3 with one lane per ciphertext.
@@ -1145,13 +1290,14 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
-// 6 = K4a with CTA-shared work (K4d). HQC_DEC_KERNEL=1..6 overrides (experiments and tests).
+// 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p).
+// HQC_DEC_KERNEL=1..7 overrides (experiments and tests).
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 6 ? env : 0;
+  return env >= 1 && env <= 7 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1176,8 +1322,14 @@ template <class P> static size_t sb_max_batch(int sms) {
   const long v = env_long("HQC_SB_MAX", dflt);
   return v < 0 ? ~(size_t)0 : (size_t)v;
 }
+// K4p (a warp pair per decryption) for the tiniest batches, up to 4 decryptions per SM: one decryption
+// 10.7 vs 13.5 us, 148 11.7 vs 14.4, 512 13.2 vs 14.2; from 1,024 (7 per SM) K4s is faster again
+// (17.7 vs 19.4 us: the SM's shared memory is saturated by the products either way and the pair's barriers
+// and idle second warp in stage 3 cost more than the halved stage 2; profiles/r02/ab_sp.log).
+template <class P> static size_t sp_max_batch(int sms) { return (size_t)env_long("HQC_SP_MAX", (long)sms * 4); }
 template <class P> static int dec_kernel_for(int sms, size_t batch) {
   if (dec_kernel_env()) return dec_kernel_env();
+  if (batch <= sp_max_batch<P>(sms)) return 7;
   return batch <= sb_max_batch<P>(sms) ? 5 : dec_kernel<P>();
 }
 // The largest group (warps per CTA) of K4s whose shared memory fits one CTA.
@@ -1222,6 +1374,12 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaFuncSetAttribute(k_decrypt_ws<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt_ws<P>, 128, decrypt_ws_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt_ws[P::level] = c > 0 ? c : 1;
+  {
+    uint32_t q = SpSmem<P>::MAX_PAIRS;
+    while (q > 1 && SpSmem<P>::bytes(q) > 227u * 1024u) q--;
+    if ((e = cudaFuncSetAttribute(k_decrypt_sp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SpSmem<P>::bytes(q))) != cudaSuccess) return e;
+  }
   if ((e = cudaFuncSetAttribute(k_decrypt_wd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1253,6 +1411,20 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     const size_t cap = (size_t)di.sms * (227u * 1024u / SbSmem<P>::bytes((uint32_t)g) > 0
                                              ? 227u * 1024u / SbSmem<P>::bytes((uint32_t)g) : 1u);
     *grid = (int)(groups < cap ? groups : cap);
+    return;
+  }
+  if (kind == 7) {  // pairs of warps, one decryption each; *per = pairs per CTA
+    constexpr uint32_t maxp = [] {
+      uint32_t q = SpSmem<P>::MAX_PAIRS;
+      while (q > 1 && SpSmem<P>::bytes(q) > 227u * 1024u) q--;
+      return q;
+    }();
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > maxp) g = maxp;
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
     return;
   }
   if (kind == 6) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
@@ -1314,6 +1486,9 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       break;
     case 6:
       k_decrypt_wd<P><<<grid, 32 * (unsigned)per, WdSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      break;
+    case 7:
+      k_decrypt_sp<P><<<grid, 64 * (unsigned)per, SpSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
       break;
     case 5:
       k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
@@ -1473,7 +1648,8 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
-  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : (kind == 5 || kind == 6) ? (int)per : 4;
+  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : (kind == 5 || kind == 6) ? (int)per
+        : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

@@ -235,7 +235,8 @@ KERNEL_NAMES = {1: "k_decrypt_w1 (fused, one warp per ciphertext range, lane-per
                 2: "k_decrypt (fused, warp pair)", 3: "k_decrypt_ws (fused, warp-specialised)",
                 4: "k_decrypt_t (fused, tensor-memory product)",
                 5: "k_decrypt_sb (fused, one warp per ciphertext, warp-parallel RS)",
-                6: "k_decrypt_wd (fused, chunks of 32 per warp, CTA-shared work counter, lane-per-word RS)"}
+                6: "k_decrypt_wd (fused, chunks of 32 per warp, CTA-shared work counter, lane-per-word RS)",
+                7: "k_decrypt_sp (fused, warp pair per ciphertext, small batches)"}
 
 
 def hqc_decrypt_launch_kernel(level: int, batch: int) -> int:
