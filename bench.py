@@ -688,6 +688,10 @@ def main():
     from paper_2512_12904_b200 import hqc
 
     world, rank, local = dist_setup()
+    # HQC_BENCH_BACKEND=gloo exercises the N > 1 host logic with all ranks on the visible GPU(s) (a check
+    # of the multi-rank code path on a one-GPU box; its timings mean nothing). The product run is NCCL.
+    backend = os.environ.get("HQC_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -695,7 +699,10 @@ def main():
         # saw all N ranks
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     p = hqc.params(args.level)
     B = args.batch
     i0, B = hdist.shard(rank, B)  # this rank's shard of the seeded workload (weak scaling)

@@ -35,6 +35,8 @@ def max_over_ranks(value: float, device=None) -> float:
 
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
+    if dist.get_backend() == "gloo":  # gloo reduces host tensors
+        device = "cpu"
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -47,6 +49,8 @@ def sum_over_ranks(count, device=None) -> int:
 
     t = count if isinstance(count, torch.Tensor) else torch.tensor([int(count)], dtype=torch.int64, device=device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.get_backend() == "gloo":  # gloo reduces host tensors
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
 
