@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "async_copy.cuh"
+#include "exp_timing.cuh"
 #include "gf256.cuh"
 #include "levels.cuh"
 #include "stage1.cuh"
@@ -358,14 +359,21 @@ template <class P> struct Enc2Smem {
   static constexpr uint32_t GF8_BYTES = sizeof(Gf8Tables);  // the encoder's log/antilog (warp 1), per CTA
   static constexpr uint32_t W0_BYTES = EU_BYTES + OUT_BYTES + SUPS_BYTES;
   static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + SUPS_BYTES + MISC_BYTES;
-  static constexpr uint32_t BYTES = GF8_BYTES + W0_BYTES + W1_BYTES;
+  static constexpr uint32_t WARP_BYTES = W0_BYTES > W1_BYTES ? W0_BYTES : W1_BYTES;
+  static constexpr uint32_t CTR_BYTES = 16;  // the CTA's two work counters (u jobs, v jobs)
+  // a CTA of Q u-warps and Q v-warps: Q <= 8 (512 threads, <= 128 registers) — 11 for HQC-1, whose warps
+  // need 91 registers (704 threads, <= 93) — and fewer where shared memory ends (HQC-3: 7, HQC-5: 4)
+  static constexpr uint32_t bytes(uint32_t q) { return GF8_BYTES + CTR_BYTES + 2 * q * WARP_BYTES; }
+  static constexpr uint32_t fit(uint32_t q) { return q > 1 && bytes(q) > 227u * 1024u ? fit(q - 1) : q; }
+  static constexpr uint32_t MAX_Q = fit(P::level == 1 ? 11 : 8);
+  static constexpr uint32_t BYTES = bytes(1);
 };
 
 #ifndef HQC_ENC2_MINB
 #define HQC_ENC2_MINB 1
 #endif
 template <class P, bool CMP = false>
-__global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
+__global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encrypt2(const uint64_t *__restrict__ h, const uint64_t *__restrict__ s,
                                                  const uint32_t *__restrict__ key_index, const uint8_t *__restrict__ m,
                                                  const uint32_t *__restrict__ r1, const uint32_t *__restrict__ r2,
                                                  const uint32_t *__restrict__ e, uint64_t *__restrict__ u_out,
@@ -375,9 +383,19 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
                                                  uint8_t *__restrict__ eq2_out = nullptr) {
   extern __shared__ __align__(16) uint8_t smem[];
   using M = Enc2Smem<P>;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // Q u-warps (role 0: u = r1 + h r2) and Q v-warps (role 1: v = mG + s r2 + e); each warp caches the
+  // doubled operand of its current key and takes jobs of its role from the CTA's contiguous range through a
+  // shared-memory counter (claimed one ahead for the TMA prefetch). With one warp pair per CTA and fixed
+  // ranges, the CTAs sharing an SM ended up to 50% apart (profiles/r02/enc_span.log): the SM ran its tail
+  // with few warps.
+  const uint32_t Q = blockDim.x >> 6;
+  const uint32_t w_all = threadIdx.x >> 5;
+  const int wid = w_all >= Q ? 1 : 0;      // role
+  const uint32_t widx = w_all - wid * Q;  // index among the warps of this role
   Gf8Tables *gf8 = reinterpret_cast<Gf8Tables *>(smem);
-  uint8_t *base = smem + M::GF8_BYTES + (wid ? M::W0_BYTES : 0u);
+  unsigned int *ctr = reinterpret_cast<unsigned int *>(smem + M::GF8_BYTES);
+  uint8_t *base = smem + M::GF8_BYTES + M::CTR_BYTES + (size_t)w_all * M::WARP_BYTES;
   uint32_t *E = reinterpret_cast<uint32_t *>(base);
   uint32_t *out = reinterpret_cast<uint32_t *>(base + (wid ? M::EV_BYTES : M::EU_BYTES));
   uint32_t *sups = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(out) + M::OUT_BYTES);
@@ -386,7 +404,7 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
   uint8_t *msg = cw + P::N1;
   const size_t lo = (size_t)blockIdx.x * per;
   const size_t hi = lo + per < batch ? lo + per : batch;
-  const uint32_t *xsrc = wid ? e : r1;  // r1 (warp 0) or e (warp 1)
+  const uint32_t *xsrc = wid ? e : r1;  // r1 (u-warps) or e (v-warps)
   constexpr uint32_t SB = P::E_STRIDE * 4;
   // buffer b: r2 row at sups + 2 b SUP, the r1 / e row at sups + (2 b + 1) SUP; mbarrier bar[b]
   auto sup_r2 = [&](int b) { return sups + (2 * b) * (M::SUP_BYTES / 4); };
@@ -404,19 +422,25 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
     if (!CMP && lane == 0) tma_store_wait_read();
     __syncwarp();
   };
+  WARP_SPAN(0, (size_t)blockIdx.x * 2 * Q + w_all);
   if (lane == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
   }
+  if (threadIdx.x == 0) ctr[0] = ctr[1] = Q;  // the first Q jobs of each role are taken statically
   for (uint32_t i = threadIdx.x; i < sizeof(Gf8Tables) / 16; i += blockDim.x)
     reinterpret_cast<uint4 *>(gf8)[i] = __ldg(reinterpret_cast<const uint4 *>(&g_gf8) + i);
   __syncthreads();
   uint32_t ph0 = 0, ph1 = 0;
-  uint32_t mnext = (wid && lo < hi && (uint32_t)lane < P::K) ? m[lo * P::K + lane] : 0u;
-  if (lo < hi) prefetch(lo, 0);
+  size_t ct = lo + widx;
+  uint32_t mnext = (wid && ct < hi && (uint32_t)lane < P::K) ? m[ct * P::K + lane] : 0u;
+  if (ct < hi) prefetch(ct, 0);
   size_t cached = ~(size_t)0;
-  for (size_t ct = lo; ct < hi; ct++) {
-    const int b = (int)((ct - lo) & 1);
+  for (int b = 0; ct < hi; b ^= 1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(ctr + wid, 1u);
+    const size_t nct = lo + __shfl_sync(0xffffffffu, nx, 0);
+    const bool more = nct < hi;
     const size_t key = key_index ? key_index[ct] : ct;
     if (key != cached) {  // a public index: the only data-dependent branch, on public data
       out_free();
@@ -426,20 +450,20 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       else s1_build_E<P, typename M::SU>(out, E, lane);
       cached = key;
     }
-    if (wid) {  // this ciphertext's message (loaded one ciphertext ahead), then the next one's
+    if (wid) {  // this ciphertext's message (loaded one job ahead), then the next one's
       if ((uint32_t)lane < P::K) msg[lane] = (uint8_t)mnext;
-      mnext = (ct + 1 < hi && (uint32_t)lane < P::K) ? m[(ct + 1) * P::K + lane] : 0u;
+      mnext = (more && (uint32_t)lane < P::K) ? m[nct * P::K + lane] : 0u;
     }
     mbar_wait(bar + b, b ? ph1 : ph0);
     if (b) ph1 ^= 1u; else ph0 ^= 1u;
-    __syncwarp();  // every lane has seen the rows land (and is done with buffer b ^ 1 of ciphertext ct - 1)
-    if (ct + 1 < hi) prefetch(ct + 1, b ^ 1);
+    __syncwarp();  // every lane has seen the rows land (and is done with buffer b ^ 1 of the previous job)
+    if (more) prefetch(nct, b ^ 1);
     uint32_t *s_r2 = sup_r2(b);
     uint32_t *s_x = sup_x(b);
     uint32_t *dsm = s_r2;  // the rotation amounts replace the r2 row entry by entry
     __syncwarp();
     uint32_t diff = 0;
-    if (wid == 0) {  // u = r1 + h * r2 (all n bits)
+    if (wid == 0) {  // u = r1 + h * r2 (all n bits)   (wid: the warp's role)
       using S = typename M::SU;
       s1_stage_d<P, S>(s_r2, dsm, lane);
       __syncwarp();
@@ -514,7 +538,9 @@ __global__ void __launch_bounds__(64, HQC_ENC2_MINB) k_encrypt2(const uint64_t *
       if (lane == 0) eq2_out[2 * ct + wid] = diff == 0;
     }
     __syncwarp();
+    ct = nct;
   }
+  WARP_SPAN(1, (size_t)blockIdx.x * 2 * Q + w_all);
   if (!CMP && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
 }
 

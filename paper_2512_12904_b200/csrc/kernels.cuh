@@ -1604,19 +1604,20 @@ static int launch_encrypt_any(const uint64_t *h, const uint64_t *s, const uint32
     k_encrypt<P, CMP><<<(unsigned)grid, 32, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch, uc, vc, eq2);
     return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
   }
-  const uint32_t smem = Enc2Smem<P>::BYTES;
-  if (cudaFuncSetAttribute(k_encrypt2<P, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+  // one CTA of Q u-warps + Q v-warps per SM, each CTA a contiguous range shared out job by job (encrypt.cuh)
+  size_t q = (batch + sms - 1) / (size_t)sms;
+  if (q < 1) q = 1;
+  if (q > Enc2Smem<P>::MAX_Q) q = Enc2Smem<P>::MAX_Q;
+  const uint32_t smem = Enc2Smem<P>::bytes((uint32_t)q);
+  if (cudaFuncSetAttribute(k_encrypt2<P, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Enc2Smem<P>::bytes(Enc2Smem<P>::MAX_Q)) != cudaSuccess)
     return HQC_ERR_CUDA;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encrypt2<P, CMP>, 64, smem) != cudaSuccess ||
-      per_sm < 1)
-    return HQC_ERR_CUDA;
-  const size_t cap = (size_t)sms * per_sm;
-  size_t ctas = (batch + 7) / 8;  // at least 8 ciphertexts per CTA
-  if (ctas > cap) ctas = cap;
+  size_t ctas = (batch + q - 1) / q;
+  if (ctas > (size_t)sms) ctas = sms;
   const size_t per = (batch + ctas - 1) / ctas;
   const size_t grid = (batch + per - 1) / per;
-  k_encrypt2<P, CMP><<<(unsigned)grid, 64, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch, per, uc, vc, eq2);
+  k_encrypt2<P, CMP><<<(unsigned)grid, 64 * (unsigned)q, smem, st>>>(h, s, key, m, r1, r2, e, u, v, batch, per, uc,
+                                                                   vc, eq2);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
