@@ -361,11 +361,11 @@ template <class P> struct Enc2Smem {
   static constexpr uint32_t W1_BYTES = EV_BYTES + OUT_BYTES + SUPS_BYTES + MISC_BYTES;
   static constexpr uint32_t WARP_BYTES = W0_BYTES > W1_BYTES ? W0_BYTES : W1_BYTES;
   static constexpr uint32_t CTR_BYTES = 16;  // the CTA's two work counters (u jobs, v jobs)
-  // a CTA of Q u-warps and Q v-warps: Q <= 8 (512 threads, <= 128 registers) — 11 for HQC-1, whose warps
-  // need 91 registers (704 threads, <= 93) — and fewer where shared memory ends (HQC-3: 7, HQC-5: 4)
+  // a CTA of Q u-warps and Q v-warps: Q <= 8 (512 threads, <= 128 registers) — 12 for HQC-1, whose warps
+  // need 80 registers (768 threads, <= 85) — and fewer where shared memory ends (HQC-3: 7, HQC-5: 4)
   static constexpr uint32_t bytes(uint32_t q) { return GF8_BYTES + CTR_BYTES + 2 * q * WARP_BYTES; }
   static constexpr uint32_t fit(uint32_t q) { return q > 1 && bytes(q) > 227u * 1024u ? fit(q - 1) : q; }
-  static constexpr uint32_t MAX_Q = fit(P::level == 1 ? 11 : 8);
+  static constexpr uint32_t MAX_Q = fit(P::level == 1 ? 12 : 8);
   static constexpr uint32_t BYTES = bytes(1);
 };
 
