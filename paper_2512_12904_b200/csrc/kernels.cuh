@@ -178,31 +178,47 @@ constexpr uint32_t GF_BYTES = round_up(sizeof(GfTables), 16);
 constexpr int WARPS_PER_CTA_S1 = 1;  // stage-1 kernel CTA size (warps)
 
 // ------------------------------------------------------------------------------------------------
-// K1: stage 1 alone. One warp per ciphertext (grid-stride over warps), on the pipe of k_decrypt_sb
-// (SbPipe, defined with it below): u lands by TMA in E's lower half, r is formed in the staging buffer and
-// leaves by a TMA bulk store, and the next u is fetched into E as soon as the product has read it.
+// K1: stage 1 alone. One warp per ciphertext at a time, on the pipe of k_decrypt_sb (SbPipe, defined with
+// it below): u lands by TMA in E's lower half, r is formed in the staging buffer and leaves by a TMA bulk
+// store, and the next u is fetched into E as soon as the product has read it. One CTA of G warps per SM
+// owns a contiguous range and its warps take products from it through a shared-memory counter (the
+// one-warp CTAs of round 1 with strided ranges left each SM a tail of few warps).
 #ifndef HQC_S1K_MINB
-#define HQC_S1K_MINB 1  // lets the compiler keep loads ahead (HQC-3 standalone product -4%)
+#define HQC_S1K_MINB 1
 #endif
 template <class P> struct SbPipe;
 template <class P> struct SbPipeSmem;
+template <class P> struct S1kSmem {
+  static constexpr uint32_t bytes(uint32_t g);
+  static constexpr uint32_t fit(uint32_t g);
+};
 template <class P>
-__global__ void __launch_bounds__(32 * WARPS_PER_CTA_S1, HQC_S1K_MINB) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
+__global__ void __launch_bounds__(512, HQC_S1K_MINB) k_stage1(const uint64_t *__restrict__ u, const uint32_t *__restrict__ y,
                                                 const uint64_t *__restrict__ v, uint64_t *__restrict__ r_out,
                                                 size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  SbPipe<P> pipe(smem + (size_t)wib * SbPipeSmem<P>::BYTES, u, v, y, lane);
-  const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
-  size_t ct = (size_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (ct < batch) pipe.issue_uy(ct, lane);
-  for (; ct < batch; ct += nwarps) {
+  const uint32_t G = blockDim.x >> 5;
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem);
+  SbPipe<P> pipe(smem + 16 + (size_t)wib * SbPipeSmem<P>::BYTES, u, v, y, lane);
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) pipe.issue_uy(ct, lane);
+  if (threadIdx.x == 0) *next_item = G;
+  __syncthreads();
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
     if (lane == 0) tma_store_wait_read();  // the previous r (in the staging buffer) has been read by its store
     __syncwarp();
-    pipe.run(ct, ct + nwarps < batch, ct + nwarps, lane);
+    pipe.run(ct, nct < c1, nct, lane);
     fence_proxy_async_smem();  // r -> HBM by a TMA bulk store, asynchronous to the next product
     __syncwarp();
     if (lane == 0) tma_store_1d(r_out + ct * P::V_WORDS, pipe.stg, P::V_WORDS * 8);
+    ct = nct;
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -642,6 +658,11 @@ template <class P> struct SbSmem {
   static constexpr uint32_t CTR_BYTES = 16;  // the CTA's work counter
   static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + CTR_BYTES + g * WARP_BYTES; }
 };
+
+template <class P> constexpr uint32_t S1kSmem<P>::bytes(uint32_t g) { return 16 + g * SbPipeSmem<P>::BYTES; }
+template <class P> constexpr uint32_t S1kSmem<P>::fit(uint32_t g) {
+  return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g;
+}
 
 template <class P>
 __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const uint64_t *__restrict__ u,
@@ -1352,7 +1373,8 @@ template <class P> static int stage1_kernel() {
   if (env == 1 || env == 2 || env == 3) return env;
   return P::level == 5 ? 2 : 1;
 }
-template <class P> static uint32_t stage1_smem() { return WARPS_PER_CTA * SbPipeSmem<P>::BYTES; }
+template <class P> static uint32_t stage1_g() { return S1kSmem<P>::fit(16); }
+template <class P> static uint32_t stage1_smem() { return S1kSmem<P>::bytes(stage1_g<P>()); }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }
@@ -1384,7 +1406,7 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
                                 WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 SbSmem<P>::bytes(sb_max_g<P>()))) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * WARPS_PER_CTA, stage1_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * stage1_g<P>(), stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   di.ready[P::level] = true;
   return cudaSuccess;
@@ -1544,10 +1566,12 @@ static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v
     k_stage1p<P><<<(unsigned)grid, 64, smem, st>>>(u, y, v, r, batch);
     return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
   }
-  const size_t cap = (size_t)di->sms * di->cap_stage1[P::level];
-  size_t grid = (batch + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-  if (grid > cap) grid = cap;
-  k_stage1<P><<<(unsigned)grid, 32 * WARPS_PER_CTA, stage1_smem<P>(), st>>>(u, y, v, r, batch);
+  size_t g = (batch + di->sms - 1) / (size_t)di->sms;  // warps per CTA: spread small batches over the SMs
+  if (g < 1) g = 1;
+  if (g > stage1_g<P>()) g = stage1_g<P>();
+  size_t grid = (batch + g - 1) / g;
+  if (grid > (size_t)di->sms) grid = di->sms;
+  k_stage1<P><<<(unsigned)grid, 32 * (unsigned)g, S1kSmem<P>::bytes((uint32_t)g), st>>>(u, y, v, r, batch);
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
