@@ -449,9 +449,9 @@ def standalone_product(args, dev, world, rank, hdist, hqc):
         val = world * B / (ms / 1e3)
         nbytes = 8 * p.u_stride + 4 * p.y_stride + 8 * p.v_words
         kern = int(os.environ.get("HQC_S1_KERNEL", "0") or 0)  # the library's choice (kernels.cuh: stage1_kernel)
-        kern = kern if kern in (1, 2, 3) else (2 if level == 5 else 1)
+        kern = kern if kern in (1, 2, 3) else 1
         res[f"n={p.n},w={p.w}"] = {"value": val, "unit": "products/s", "batch_per_gpu": B, "ms_per_step": ms,
-                                   "kernel": {1: "k_stage1 (one warp, windows from shared memory)",
+                                   "kernel": {1: "k_stage1 (one warp per product, CTA-shared work, windows from shared memory)",
                                               2: "k_stage1p (warp pair, windows from shared memory)",
                                               3: "k_stage1t (windows from tensor memory)"}[kern],
                                    "alu_roofline_frac": val / world * ops["stage1"] / peak,

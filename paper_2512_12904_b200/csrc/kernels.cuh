@@ -1371,7 +1371,9 @@ template <class P> static int stage1_kernel() {
     return s ? atoi(s) : 0;
   }();
   if (env == 1 || env == 2 || env == 3) return env;
-  return P::level == 5 ? 2 : 1;
+  // round 2: k_stage1 with the CTA-shared work counter beats the warp pair at HQC-5 too (1.847 vs 2.117 ms
+  // per 65,536, profiles/r02/ab_s1_l5.log)
+  return 1;
 }
 template <class P> static uint32_t stage1_g() { return S1kSmem<P>::fit(16); }
 template <class P> static uint32_t stage1_smem() { return S1kSmem<P>::bytes(stage1_g<P>()); }

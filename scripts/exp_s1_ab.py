@@ -28,8 +28,15 @@ for c in sys.argv[2].split(","):
 '''.replace("ROOT", ROOT)
 
 if __name__ == "__main__":
+    # an argument "S1=k@LIB" runs LIB with HQC_S1_KERNEL=k
     for rep in range(2):
         for lib in sys.argv[1:3]:
-            r = subprocess.run([sys.executable, "-c", CODE, lib, sys.argv[3]], capture_output=True, text=True, cwd=ROOT)
+            env = dict(os.environ)
+            if "@" in lib:
+                kv, lib = lib.split("@")
+                env["HQC_S1_KERNEL"] = kv.split("=")[1]
+                sys.stdout.write(f"# HQC_S1_KERNEL={env['HQC_S1_KERNEL']}\n")
+            r = subprocess.run([sys.executable, "-c", CODE, lib, sys.argv[3]], capture_output=True, text=True, cwd=ROOT,
+                               env=env)
             sys.stdout.write(r.stdout + (r.stderr[-2000:] if r.returncode else ""))
             sys.stdout.flush()
