@@ -521,6 +521,163 @@ __global__ void __launch_bounds__(32 * WdSmem<P>::MAX_G, 1) k_decrypt_wd(const u
 }
 
 
+// K4l: the lane-per-word RS decoder of K4a/K4d in a COMPACT per-warp layout. K4s (one warp per decryption,
+// warp RS) needs a staging buffer for v next to E; K4d (chunks of 32, lane RS) needs the symbol chunk on top
+// of K4a's staging buffers — neither leaves room for 16 warps per SM at HQC-3. Here v is not staged: it is
+// fetched (TMA) after the product, into the part of E above u's row, which the product no longer needs,
+// r is formed there in place, stage 2 reads it there, and the chunk's RS scratch reuses it; meanwhile the
+// next u lands below it. Per warp: E, the support row, the rotation amounts, the symbol chunk — HQC-3
+// 11.8 KB (16 warps per SM), HQC-5 19.3 KB (11). The CTA's warps share its range through a counter (K4d).
+// The v fetch is not hidden behind this warp's product (it cannot land earlier); other warps hide it.
+template <class P> struct WlSmem {
+  using S = DecShape<P>;
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t RB = VB > S3Scratch<P>::BYTES ? VB : S3Scratch<P>::BYTES;  // v, r, RS scratch
+  static constexpr uint32_t E_BYTES = round_up(S::E_WORDS * 4 > UB + RB ? S::E_WORDS * 4 : UB + RB, 16);
+  static constexpr uint32_t Y_BYTES = round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t SYM_PITCH = 36;
+  static constexpr uint32_t SYM_BYTES = round_up(P::N1 * SYM_PITCH, 16);
+  static constexpr uint32_t IDX_BYTES = 32 * 4;
+  static constexpr uint32_t WARP_BYTES = E_BYTES + Y_BYTES + D_BYTES + SYM_BYTES + IDX_BYTES + 16;
+  static constexpr uint32_t bytes(uint32_t g) { return GF_BYTES + 16 + g * WARP_BYTES; }
+  static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
+  static constexpr uint32_t MAX_G = fit(16);
+  static_assert(UB % 16 == 0, "the v / r region starts 16-byte aligned above u's row");
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out,
+                                                                        size_t batch) {
+  using M = WlSmem<P>;
+  using S = DecShape<P>;
+  using ST = DecShapeT<P>;
+  constexpr uint32_t TW = dec_tail_words<P>();
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem + GF_BYTES);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t G = blockDim.x >> 5;
+  uint8_t *ws = smem + GF_BYTES + 16 + (size_t)wib * M::WARP_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
+  uint32_t *Rv = reinterpret_cast<uint32_t *>(ws + M::UB);  // v, then r, then the RS scratch
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::Y_BYTES);
+  uint8_t *sb = ws + M::E_BYTES + M::Y_BYTES + M::D_BYTES;
+  uint32_t *cidx = reinterpret_cast<uint32_t *>(sb + M::SYM_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sb + M::SYM_BYTES + M::IDX_BYTES);  // [0] u, y  [1] v
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncwarp();
+  auto issue_uy = [&](size_t c) {
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, M::UB + M::YB);
+      tma_load_1d(E, u + c * P::U_STRIDE, M::UB, bar);
+      tma_load_1d(stg_y, y + c * P::Y_STRIDE, M::YB, bar);
+    }
+  };
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) issue_uy(ct);
+  if (threadIdx.x == 0) *next_item = G;
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  uint32_t ph_uy = 0, ph_v = 0, slot = 0;
+  constexpr uint32_t MASK_C = (1u << P::C) - 1u;
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    const bool more = nct < c1;
+    mbar_wait(bar, ph_uy);
+    ph_uy ^= 1u;
+    s1_stage_d<P, S>(stg_y, dsm, lane);
+    {  // E's shifted upper copy from u's row in its lower half (as SbPipe::build_E)
+      constexpr uint32_t NF = P::Q0 - 1;
+      constexpr uint32_t CH = ((NF + 31) / 32) | 1u;
+      uint32_t eq0 = 0, s0 = 0, sl = 0;
+      if (lane == 0) {
+        eq0 = E[P::Q0] & MASK_C;
+        s0 = E[0];
+        sl = E[P::Q0 - 1];
+      }
+      const uint32_t x0 = (uint32_t)lane * CH;
+      uint32_t lo = x0 < NF ? E[x0] : 0u;
+#pragma unroll 4
+      for (uint32_t t = 0; t < CH; t++) {
+        const uint32_t x = x0 + t;
+        if (x < NF) {
+          const uint32_t hi = E[x + 1];
+          E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+          lo = hi;
+        }
+      }
+      if (lane == 0) {
+        E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);
+        E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);
+        E[P::Q0] = eq0 | (s0 << P::C);
+      }
+      for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
+    }
+    __syncwarp();
+    uint32_t acc[ST::R];
+    s1_product<P, ST>(E, dsm, acc, lane);
+    uint32_t mine = 0;
+    if constexpr (TW > 0) {
+      uint32_t t[TW];
+      s1_tail_words<P, ST, ST::NOUT, TW>(E, dsm, lane, t);
+#pragma unroll
+      for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
+    }
+    __syncwarp();  // E is read: v may land above u's row, the next u in it
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar + 1, M::VB);
+      tma_load_1d(Rv, v + ct * P::V_WORDS, M::VB, bar + 1);
+    }
+    if (more) issue_uy(nct);
+    if (lane == 0) cidx[slot] = (uint32_t)(ct - c0);
+    mbar_wait(bar + 1, ph_v);
+    ph_v ^= 1u;
+    s1_store_r_xor<ST>(acc, Rv, Rv, lane);  // r = acc ^ v in place
+    if (TW > 0 && (uint32_t)lane < TW) Rv[ST::NOUT + lane] = mine ^ Rv[ST::NOUT + lane];
+    __syncwarp();
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2 into the chunk's slot
+      const uint4 *src = reinterpret_cast<const uint4 *>(Rv) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      sb[j * M::SYM_PITCH + slot] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+    __syncwarp();
+    slot++;
+    if (slot == 32 || !more) {  // stage 3, lane per word, scratch above u's row
+      for (uint32_t q = slot; q < 32; q++)
+        for (uint32_t j = lane; j < P::N1; j += 32) sb[j * M::SYM_PITCH + q] = 0;
+      __syncwarp();
+      const bool act = (uint32_t)lane < slot;
+      auto sym_at = [&](int j) -> uint32_t { return sb[j * M::SYM_PITCH + lane]; };
+      rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(Rv), lane,
+                        act ? m_out + (c0 + cidx[lane]) * P::K : nullptr);
+      __syncwarp();
+      slot = 0;
+    }
+    ct = nct;
+  }
+}
+
+
 // K4s: fused decrypt for SMALL batches (BASELINE configs[0]: HQC-1 at 1,024). K4a gives every warp at
 // least 16 consecutive ciphertexts, so a batch of 1,024 occupies 64 warps on 64 SMs and the launch is the
 // latency of 16 products in a row plus a lane-per-word RS decode. Here every warp takes ONE ciphertext at a
@@ -1311,21 +1468,21 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
-// 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p).
-// HQC_DEC_KERNEL=1..7 overrides (experiments and tests).
+// 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p),
+// 8 = compact lane-RS warps (K4l). HQC_DEC_KERNEL=1..8 overrides (experiments and tests).
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 7 ? env : 0;
+  return env >= 1 && env <= 8 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
   // above the K4s range: HQC-1 K4d (65,536: 0.526 vs 0.560 ms for K4a; 262,144: +6.7%,
-  // profiles/r02/ab_wd.log), HQC-5 K4a (K4d -3%: 8 warps per SM either way, and K4d's 239 registers per
-  // thread buy nothing there); HQC-3 never gets here (K4s at every batch)
-  return P::level == 1 ? 6 : P::level == 3 ? 2 : 1;
+  // profiles/r02/ab_wd.log), HQC-3 K4l (65,536: 1.073 vs 1.139 ms for K4s, profiles/r02/ab_wl.log; K4d fits
+  // only 13 warps there), HQC-5 K4a (K4d -5.5%, K4l -2.4..-5%: its de-phased warps contend harder)
+  return P::level == 1 ? 6 : P::level == 3 ? 8 : 1;
 }
 // Read on every call (experiments sweep them within one process): HQC_SB_MAX = the largest batch that
 // takes K4s by default; HQC_DEC_SPLIT = the most ciphertexts one launch of the large-batch kernels takes.
@@ -1339,7 +1496,9 @@ static long env_long(const char *name, long dflt) {
 // RM stage and lane-per-word RS win); HQC-5 up to ~24,000 (16,384: 2.41e7 vs 2.24e7; 32,768: 2.37e7 vs
 // 2.58e7 — its shared memory allows 10 warps per SM in K4s, 8 in K4a but with the cheaper lane RS).
 template <class P> static size_t sb_max_batch(int sms) {
-  const long dflt = P::level == 3 ? -1L : (long)sms * (P::level == 1 ? 270 : 160);
+  // HQC-3: K4s up to ~44,000, K4l beyond (32,768: 0.591 vs 0.600 ms; 65,536: 1.139 vs 1.073;
+  // 4,194,304: 6.05e7 vs 6.36e7/s — profiles/r02/ab_wl*.log)
+  const long dflt = (long)sms * (P::level == 1 ? 270 : P::level == 3 ? 300 : 160);
   const long v = env_long("HQC_SB_MAX", dflt);
   return v < 0 ? ~(size_t)0 : (size_t)v;
 }
@@ -1404,6 +1563,8 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
     if ((e = cudaFuncSetAttribute(k_decrypt_sp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SpSmem<P>::bytes(q))) != cudaSuccess) return e;
   }
+  if ((e = cudaFuncSetAttribute(k_decrypt_wl<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WlSmem<P>::bytes(WlSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_wd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1446,6 +1607,15 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > maxp) g = maxp;
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
+    return;
+  }
+  if (kind == 8) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > WlSmem<P>::MAX_G) g = WlSmem<P>::MAX_G;
     *per = g;
     const size_t groups = (batch + g - 1) / g;
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
@@ -1513,6 +1683,9 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       break;
     case 7:
       k_decrypt_sp<P><<<grid, 64 * (unsigned)per, SpSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      break;
+    case 8:
+      k_decrypt_wl<P><<<grid, 32 * (unsigned)per, WlSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
       break;
     case 5:
       k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
@@ -1675,8 +1848,8 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   size_t per;
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
-  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS : (kind == 5 || kind == 6) ? (int)per
-        : kind == 7 ? 2 * (int)per : 4;
+  *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
+        : (kind == 5 || kind == 6 || kind == 8) ? (int)per : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 
