@@ -546,7 +546,9 @@ template <class P> struct WlSmem {
   static_assert(UB % 16 == 0, "the v / r region starts 16-byte aligned above u's row");
 };
 
-template <class P>
+// DYNAMIC = false: each warp owns a contiguous share of the CTA's range instead (warps stay in phase, as in
+// K4a — what HQC-5's 8.6k-instruction kernel prefers, profiles/r02/ab_wd5.log).
+template <class P, bool DYNAMIC = true>
 __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const uint64_t *__restrict__ u,
                                                                         const uint64_t *__restrict__ v,
                                                                         const uint32_t *__restrict__ y,
@@ -583,9 +585,16 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     }
   };
   const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
-  const size_t c0 = (size_t)blockIdx.x * per_cta;
-  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
-  size_t ct = c0 + wib;
+  size_t c0 = (size_t)blockIdx.x * per_cta;
+  size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  const size_t cbase = c0;  // chunk indices are relative to the CTA's range
+  if constexpr (!DYNAMIC) {  // this warp's contiguous share
+    const size_t n = c1 > c0 ? c1 - c0 : 0, pw = (n + G - 1) / G;
+    const size_t w0 = c0 + (size_t)wib * pw;
+    c0 = w0 < c1 ? w0 : c1;
+    c1 = c0 + pw < c1 ? c0 + pw : c1;
+  }
+  size_t ct = DYNAMIC ? c0 + wib : c0;
   if (ct < c1) issue_uy(ct);
   if (threadIdx.x == 0) *next_item = G;
   gf_tables_to_smem(gf);
@@ -593,9 +602,12 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
   uint32_t ph_uy = 0, ph_v = 0, slot = 0;
   constexpr uint32_t MASK_C = (1u << P::C) - 1u;
   while (ct < c1) {
-    uint32_t nx = 0;
-    if (lane == 0) nx = atomicAdd(next_item, 1u);
-    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    size_t nct = ct + 1;
+    if constexpr (DYNAMIC) {
+      uint32_t nx = 0;
+      if (lane == 0) nx = atomicAdd(next_item, 1u);
+      nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    }
     const bool more = nct < c1;
     mbar_wait(bar, ph_uy);
     ph_uy ^= 1u;
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
       tma_load_1d(Rv, v + ct * P::V_WORDS, M::VB, bar + 1);
     }
     if (more) issue_uy(nct);
-    if (lane == 0) cidx[slot] = (uint32_t)(ct - c0);
+    if (lane == 0) cidx[slot] = (uint32_t)(ct - cbase);
     mbar_wait(bar + 1, ph_v);
     ph_v ^= 1u;
     s1_store_r_xor<ST>(acc, Rv, Rv, lane);  // r = acc ^ v in place
@@ -669,7 +681,7 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
       const bool act = (uint32_t)lane < slot;
       auto sym_at = [&](int j) -> uint32_t { return sb[j * M::SYM_PITCH + lane]; };
       rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(Rv), lane,
-                        act ? m_out + (c0 + cidx[lane]) * P::K : nullptr);
+                        act ? m_out + (cbase + cidx[lane]) * P::K : nullptr);
       __syncwarp();
       slot = 0;
     }
@@ -1469,13 +1481,13 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
 // 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p),
-// 8 = compact lane-RS warps (K4l). HQC_DEC_KERNEL=1..8 overrides (experiments and tests).
+// 8 = compact lane-RS warps (K4l), 9 = K4l with static per-warp ranges. HQC_DEC_KERNEL=1..9 overrides.
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 8 ? env : 0;
+  return env >= 1 && env <= 9 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1563,7 +1575,9 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
     if ((e = cudaFuncSetAttribute(k_decrypt_sp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SpSmem<P>::bytes(q))) != cudaSuccess) return e;
   }
-  if ((e = cudaFuncSetAttribute(k_decrypt_wl<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if ((e = cudaFuncSetAttribute(k_decrypt_wl<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WlSmem<P>::bytes(WlSmem<P>::MAX_G))) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_decrypt_wl<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WlSmem<P>::bytes(WlSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_wd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
@@ -1612,7 +1626,7 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
     return;
   }
-  if (kind == 8) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
+  if (kind == 8 || kind == 9) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > WlSmem<P>::MAX_G) g = WlSmem<P>::MAX_G;
@@ -1685,7 +1699,10 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       k_decrypt_sp<P><<<grid, 64 * (unsigned)per, SpSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
       break;
     case 8:
-      k_decrypt_wl<P><<<grid, 32 * (unsigned)per, WlSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      k_decrypt_wl<P, true><<<grid, 32 * (unsigned)per, WlSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      break;
+    case 9:
+      k_decrypt_wl<P, false><<<grid, 32 * (unsigned)per, WlSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
       break;
     case 5:
       k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
@@ -1849,7 +1866,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
   *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
-        : (kind == 5 || kind == 6 || kind == 8) ? (int)per : kind == 7 ? 2 * (int)per : 4;
+        : (kind == 5 || kind == 6 || kind == 8 || kind == 9) ? (int)per : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

@@ -267,7 +267,7 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
     """The library picks the warp-pair kernel (HQC-3) or the one-warp kernel (HQC-1/5) per level, and the
     small-batch group kernel (5) for small batches; the warp-specialised kernel (3) and the
