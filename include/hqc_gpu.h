@@ -243,9 +243,12 @@ int hqc_decrypt_ct_batch_host(const hqc_params *p, const uint8_t *ct_h, const ui
  * (introspection for the bench's launch accounting). Returns HQC_OK. */
 int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *warps_per_cta);
 /* Which fused kernel hqc_decrypt_batch runs for `batch`: 1 = k_decrypt_w1 (one warp
- * per ciphertext range), 2 = k_decrypt (warp pair), 3 = k_decrypt_ws (warp-specialised), 4 = k_decrypt_t
- * (tensor-memory product, opt-in), 5 = k_decrypt_sb (one warp per ciphertext, warp-parallel RS);
- * negative hqc_status on error. */
+ * per ciphertext range, lane-per-word RS), 2 = k_decrypt (warp pair), 3 = k_decrypt_ws (warp-specialised),
+ * 4 = k_decrypt_t (tensor-memory product, opt-in), 5 = k_decrypt_sb (one warp per ciphertext, warp-parallel
+ * RS), 6 = k_decrypt_wd (k_decrypt_w1 with CTA-shared work), 7 = k_decrypt_sp (a warp pair per ciphertext,
+ * small batches), 8 = k_decrypt_wl (compact warps, CTA-shared work, lane-per-word RS), 9 = k_decrypt_wl with
+ * static ranges; negative hqc_status on error. The default depends on the level and the batch; the
+ * environment variable HQC_DEC_KERNEL=1..9 forces one (tests, experiments). */
 int hqc_decrypt_launch_kernel(const hqc_params *p, size_t batch);
 /* How many kernel launches hqc_decrypt_batch makes for `batch` (a large batch runs as consecutive
  * launches of at most a per-level size); negative hqc_status on error. */
