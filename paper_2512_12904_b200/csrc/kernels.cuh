@@ -600,7 +600,6 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
   gf_tables_to_smem(gf);
   __syncthreads();
   uint32_t ph_uy = 0, ph_v = 0, slot = 0;
-  constexpr uint32_t MASK_C = (1u << P::C) - 1u;
   while (ct < c1) {
     size_t nct = ct + 1;
     if constexpr (DYNAMIC) {
@@ -612,33 +611,7 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     mbar_wait(bar, ph_uy);
     ph_uy ^= 1u;
     s1_stage_d<P, S>(stg_y, dsm, lane);
-    {  // E's shifted upper copy from u's row in its lower half (as SbPipe::build_E)
-      constexpr uint32_t NF = P::Q0 - 1;
-      constexpr uint32_t CH = ((NF + 31) / 32) | 1u;
-      uint32_t eq0 = 0, s0 = 0, sl = 0;
-      if (lane == 0) {
-        eq0 = E[P::Q0] & MASK_C;
-        s0 = E[0];
-        sl = E[P::Q0 - 1];
-      }
-      const uint32_t x0 = (uint32_t)lane * CH;
-      uint32_t lo = x0 < NF ? E[x0] : 0u;
-#pragma unroll 4
-      for (uint32_t t = 0; t < CH; t++) {
-        const uint32_t x = x0 + t;
-        if (x < NF) {
-          const uint32_t hi = E[x + 1];
-          E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
-          lo = hi;
-        }
-      }
-      if (lane == 0) {
-        E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);
-        E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);
-        E[P::Q0] = eq0 | (s0 << P::C);
-      }
-      for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
-    }
+    s1_build_E_upper<P, S>(E, lane);  // the shifted upper copy of E from u's row in its lower half
     __syncwarp();
     uint32_t acc[ST::R];
     s1_product<P, ST>(E, dsm, acc, lane);
@@ -743,39 +716,8 @@ template <class P> struct SbPipe {
       tma_load_1d(stg_y, y + ct * P::Y_STRIDE, M::YB, bar);
     }
   }
-  // E from the u row already in its lower half: the shifted copy above word Q0 (E[Q0 + 1 + x] =
-  // funnel(u32[x], u32[x + 1], 32 - C), u32[Q0] masked to its C valid bits, u32[Q0 + 1] = 0), then word Q0
-  // itself (the wrap of X^n = 1) and the zero tail. Reads stay below word Q0, writes above it (lane 0 reads
-  // and rewrites word Q0 last), so no in-place hazard.
-  __device__ __forceinline__ void build_E(int lane) {
-    using S = DecShape<P>;
-    constexpr uint32_t MASK_C = (1u << P::C) - 1u;
-    constexpr uint32_t NF = P::Q0 - 1;                  // x = 0 .. Q0 - 2: both sources below word Q0
-    constexpr uint32_t CH = ((NF + 31) / 32) | 1u;      // per-lane run, odd: conflict-free
-    uint32_t eq0 = 0, s0 = 0, sl = 0;
-    if (lane == 0) {
-      eq0 = E[P::Q0] & MASK_C;
-      s0 = E[0];
-      sl = E[P::Q0 - 1];
-    }
-    const uint32_t x0 = (uint32_t)lane * CH;
-    uint32_t lo = x0 < NF ? E[x0] : 0u;
-#pragma unroll 4
-    for (uint32_t t = 0; t < CH; t++) {
-      const uint32_t x = x0 + t;
-      if (x < NF) {
-        const uint32_t hi = E[x + 1];
-        E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
-        lo = hi;
-      }
-    }
-    if (lane == 0) {
-      E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);      // x = Q0 - 1
-      E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);  // x = Q0
-      E[P::Q0] = eq0 | (s0 << P::C);
-    }
-    for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
-  }
+  // E from the u row already in its lower half (stage1.cuh: s1_build_E_upper)
+  __device__ __forceinline__ void build_E(int lane) { s1_build_E_upper<P, DecShape<P>>(E, lane); }
   // Stage 1 of ct (its u, y requested); leaves r in stg; requests next's u, y as soon as E is read.
   __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
     using S = DecShape<P>;
@@ -961,33 +903,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
     if (wa == 0) {
       mbar_wait(bar, ph_uy);
       s1_stage_d<P, S>(stg_y, dsm, lane);
-      // E from the u row in its lower half (as SbPipe::build_E)
-      constexpr uint32_t MASK_C = (1u << P::C) - 1u;
-      constexpr uint32_t NF = P::Q0 - 1;
-      constexpr uint32_t CH = ((NF + 31) / 32) | 1u;
-      uint32_t eq0 = 0, s0 = 0, sl = 0;
-      if (lane == 0) {
-        eq0 = E[P::Q0] & MASK_C;
-        s0 = E[0];
-        sl = E[P::Q0 - 1];
-      }
-      const uint32_t x0 = (uint32_t)lane * CH;
-      uint32_t lo = x0 < NF ? E[x0] : 0u;
-#pragma unroll 4
-      for (uint32_t t = 0; t < CH; t++) {
-        const uint32_t x = x0 + t;
-        if (x < NF) {
-          const uint32_t hi = E[x + 1];
-          E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
-          lo = hi;
-        }
-      }
-      if (lane == 0) {
-        E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);
-        E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);
-        E[P::Q0] = eq0 | (s0 << P::C);
-      }
-      for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
+      s1_build_E_upper<P, S>(E, lane);  // E from the u row in its lower half
       __syncwarp();
       if (lane == 0) {  // v lands in stg during the product
         fence_proxy_async_smem();

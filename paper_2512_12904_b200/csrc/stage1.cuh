@@ -113,6 +113,42 @@ __device__ __forceinline__ void s1_build_E(uint32_t *su, uint32_t *E, int lane) 
   }
 }
 
+// E from the u row that TMA put in E's LOWER half (E[q] = u32[q] for q <= Q0; k_stage1, k_decrypt_sb /
+// _sp / _wl): only the shifted upper copy is built — E[Q0 + 1 + x] = funnel(u32[x], u32[x + 1], 32 - C),
+// u32[Q0] masked to its C valid bits, u32[Q0 + 1] = 0 — then word Q0 itself (the wrap of X^n = 1) and the
+// zero tail up to S::E_WORDS. One warp; the lanes' runs read only below word Q0 and write above it, and
+// lane 0 reads word Q0 before it rewrites it, so the build is in place with no hazard.
+template <class P, class S>
+__device__ __forceinline__ void s1_build_E_upper(uint32_t *E, int lane) {
+  constexpr uint32_t MASK_C = (1u << P::C) - 1u;
+  constexpr uint32_t NF = P::Q0 - 1;              // x = 0 .. Q0 - 2: both sources below word Q0
+  constexpr uint32_t CH = ((NF + 31) / 32) | 1u;  // per-lane run, odd: conflict-free
+  static_assert(S::E_WORDS >= 2 * P::Q0 + 2, "E holds the doubled u");
+  uint32_t eq0 = 0, s0 = 0, sl = 0;
+  if (lane == 0) {
+    eq0 = E[P::Q0] & MASK_C;
+    s0 = E[0];
+    sl = E[P::Q0 - 1];
+  }
+  const uint32_t x0 = (uint32_t)lane * CH;
+  uint32_t lo = x0 < NF ? E[x0] : 0u;
+#pragma unroll 4
+  for (uint32_t t = 0; t < CH; t++) {
+    const uint32_t x = x0 + t;
+    if (x < NF) {
+      const uint32_t hi = E[x + 1];
+      E[P::Q0 + 1 + x] = __funnelshift_r(lo, hi, 32 - P::C);
+      lo = hi;
+    }
+  }
+  if (lane == 0) {
+    E[2 * P::Q0] = __funnelshift_r(sl, eq0, 32 - P::C);      // x = Q0 - 1
+    E[2 * P::Q0 + 1] = __funnelshift_r(eq0, 0u, 32 - P::C);  // x = Q0 (u32[Q0 + 1] = 0)
+    E[P::Q0] = eq0 | (s0 << P::C);
+  }
+  for (uint32_t q = 2 * P::Q0 + 2 + lane; q < S::E_WORDS; q += 32) E[q] = 0u;
+}
+
 // A rotation amount d = 32 o + s is kept as (o << 7) | s: its low 5 bits are the funnel-shift amount
 // (SHF.R.W wraps the amount mod 32) and >> 5 is the window's byte offset 4 o, one shift instead of a
 // shift and a mask per index.

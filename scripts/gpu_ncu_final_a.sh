@@ -11,11 +11,3 @@ run fused_L1 k_decrypt python scripts/prof_kernels.py --level 1 --batch 65536 --
 run fused_L3 k_decrypt python scripts/prof_kernels.py --level 3 --batch 65536 --only fused --iters 2
 run fused_L5 k_decrypt python scripts/prof_kernels.py --level 5 --batch 262144 --only fused --iters 2
 run fused_L1_1024 k_decrypt python scripts/prof_kernels.py --level 1 --batch 1024 --only fused --iters 2
-run s1n_L1 k_stage1 python scripts/prof_kernels.py --level 1 --only s1n --iters 2
-run s1n_L3 k_stage1 python scripts/prof_kernels.py --level 3 --only s1n --iters 2
-run s1n_L5 k_stage1 python scripts/prof_kernels.py --level 5 --only s1n --iters 2
-# launch list of a short bench run (headline only)
-CMD="python bench.py --steps 5 --warmup 3 --no-configs --no-levels --no-variants --no-cpu-baseline"
-timeout 600 $CMD > gpurun_out/final_bench_plain.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv $CMD > gpurun_out/final_ncu_launches.log 2>&1
-echo "launches exit $?" >> gpurun_out/final_status.log
