@@ -441,7 +441,10 @@ template <class P> struct WdSmem {
   // warps per CTA: at most 16 (512 threads, <= 128 registers), fewer where shared memory runs out
   // (HQC-3: 13 of 16.4 KB, HQC-5: 8 of 26 KB)
   static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
-  static constexpr uint32_t MAX_G = fit(16);
+#ifndef HQC_WD_G
+#define HQC_WD_G 16
+#endif
+  static constexpr uint32_t MAX_G = fit(HQC_WD_G);
 };
 
 template <class P>
