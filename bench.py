@@ -537,6 +537,21 @@ def config1_block(args, dev, world, rank, hdist, hqc, B: int = 1024) -> dict:
         e1.synchronize()
         wall.append(time.perf_counter() - t0)
         lat.append(e0.elapsed_time(e1))
+    # one launch captured alone in a graph, replayed with events around each replay: the latency of one
+    # batch of 1,024 without the host-side launch cost of a plain stream launch
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1):
+        run()
+    for _ in range(3):
+        g1.replay()
+    torch.cuda.synchronize()
+    lat_g = []
+    for _ in range(50):
+        e0.record(st)
+        g1.replay()
+        e1.record(st)
+        e1.synchronize()
+        lat_g.append(e0.elapsed_time(e1))
     G, R = 64, 10
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
@@ -557,6 +572,7 @@ def config1_block(args, dev, world, rank, hdist, hqc, B: int = 1024) -> dict:
             "alu_roofline_frac": val / world * ops / _alu_peak(dev),
             "stream_ms_per_launch": hdist.max_over_ranks(ms_stream, dev),
             "single_launch_ms": {"median": float(np.median(lat)), "min": float(min(lat)), "n": len(lat)},
+            "single_graph_launch_ms": {"median": float(np.median(lat_g)), "min": float(min(lat_g)), "n": len(lat_g)},
             "single_launch_host_wall_ms": {"median": 1e3 * float(np.median(wall)), "min": 1e3 * float(min(wall))},
             "launch": {"kernel": hqc.KERNEL_NAMES[hqc.hqc_decrypt_launch_kernel(level, B)], "grid": grid,
                        "warps_per_cta": wpc},
