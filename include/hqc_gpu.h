@@ -87,11 +87,18 @@ const char *hqc_status_str(int status);
  *   v         [batch][v_words]  uint64   ciphertext part v (n1*n2 bits)
  *   y_support [batch][y_stride] uint32   the secret y's support, first w entries used (R#1)
  *   m_out     [batch][k]        uint8    decrypted messages (RS failure -> uncorrected bytes)
- * One kernel: stage 1 in shared memory (a warp pair per ciphertext for HQC-3, one warp for
- * HQC-1/5), stage 2 lane-per-RM-block, stage 3 lane-per-ciphertext; no intermediate leaves the SM.
- * Constant-flow (R#8). HQC_DEC_KERNEL=1|2|3 forces the one-warp / pair / warp-specialised
- * variant (same results); HQC_DEC_KERNEL=4 the tensor-memory-product variant, whose loop counts
- * depend on y. The variable is read once per process.
+ * The launch policy picks the kernel by level and batch (hqc_decrypt_launch_kernel
+ * reports it): one fused kernel — stage 1 in shared memory, stage 2 lane-per-RM-block, stage 3 by a
+ * warp per word (small batches) or a lane per word (large ones), no intermediate leaving the SM — except
+ * HQC-5 at large batches (kernel 10), which runs stages 1+2 in one launch, writes the n1 received
+ * symbols of each ciphertext to a scratch buffer and decodes them in a second launch. That scratch
+ * (batch x n1 bytes, at most 1,048,576 rows per launch) comes from a memory pool the library creates
+ * per device on first use; it is stream-ordered (allocated and freed on `stream`, so concurrent calls
+ * on different streams are safe and the call can be captured in a CUDA graph) and the pool keeps freed
+ * memory for later calls (up to ~94 MB). A large batch may run as consecutive launches
+ * (hqc_decrypt_launch_count). All default kernels are constant-flow (R#8). HQC_DEC_KERNEL=1..10
+ * forces a kernel (same results; 4 is the tensor-memory product, whose loop counts depend on y,
+ * DESIGN.md §6.1b); the variable is read once per process.
  * ------------------------------------------------------------------------------------------- */
 int hqc_decrypt_batch(const hqc_params *p, const uint64_t *u, const uint64_t *v,
                       const uint32_t *y_support, uint8_t *m_out, size_t batch, void *stream);
@@ -247,11 +254,13 @@ int hqc_decrypt_launch_shape(const hqc_params *p, size_t batch, int *grid, int *
  * 4 = k_decrypt_t (tensor-memory product, opt-in), 5 = k_decrypt_sb (one warp per ciphertext, warp-parallel
  * RS), 6 = k_decrypt_wd (k_decrypt_w1 with CTA-shared work), 7 = k_decrypt_sp (a warp pair per ciphertext,
  * small batches), 8 = k_decrypt_wl (compact warps, CTA-shared work, lane-per-word RS), 9 = k_decrypt_wl with
- * static ranges; negative hqc_status on error. The default depends on the level and the batch; the
- * environment variable HQC_DEC_KERNEL=1..9 forces one (tests, experiments). */
+ * static ranges, 10 = k_decrypt_s12 + k_stage3 (stages 1+2, then stage 3 lane-per-word: two launches);
+ * negative hqc_status on error. The default depends on the level and the batch; the environment variable
+ * HQC_DEC_KERNEL=1..10 forces one (tests, experiments). */
 int hqc_decrypt_launch_kernel(const hqc_params *p, size_t batch);
 /* How many kernel launches hqc_decrypt_batch makes for `batch` (a large batch runs as consecutive
- * launches of at most a per-level size); negative hqc_status on error. */
+ * launches of at most a per-level size; kernel 10 is two launches per part); negative
+ * hqc_status on error. */
 long long hqc_decrypt_launch_count(const hqc_params *p, size_t batch);
 
 #ifdef __cplusplus

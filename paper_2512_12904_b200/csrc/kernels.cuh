@@ -835,6 +835,52 @@ __global__ void __launch_bounds__(32 * SbSmem<P>::MAX_G, 1) k_decrypt_sb(const u
   WARP_SPAN(1, (size_t)blockIdx.x * G + wib);
 }
 
+// K4x (round 2, HQC-5 at large batches): the decrypt as TWO launches — this kernel runs stages 1 and 2 on
+// the pipe of k_stage1 (a CTA of up to 16 warps per SM, 128 registers, the CTA-shared work counter) and
+// writes each ciphertext's n1 received symbols to a scratch row in HBM; k_stage3 then decodes them 32 per
+// warp with the lane-per-word RS decoder. HQC-5's lane decoder needs ~240 registers, which held the fused
+// kernels to 8 warps per SM, and its chunks left the shared-memory pipe idle while they ran; split, the
+// product runs at k_stage1's occupancy and the decoder at its own (profiles/r02/time_stages.log: three
+// separate stage launches already beat the fused K4a at 262,144, 9.15 vs 9.57 ms). The symbols cost
+// n1 bytes per ciphertext of HBM each way.
+template <class P>
+__global__ void __launch_bounds__(512, 1) k_decrypt_s12(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
+                                                        const uint32_t *__restrict__ y, uint8_t *__restrict__ sym_out,
+                                                        size_t batch, uint32_t stagger_ns) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t G = blockDim.x >> 5;
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem);
+  SbPipe<P> pipe(smem + 16 + (size_t)wib * SbPipeSmem<P>::BYTES, u, v, y, lane);
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) pipe.issue_uy(ct, lane);
+  if (threadIdx.x == 0) *next_item = G;
+  __syncthreads();
+  if (stagger_ns) __nanosleep(stagger_ns * (uint32_t)wib);  // experiments: de-phase the warps of a CTA
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    pipe.run(ct, nct < c1, nct, lane);
+    uint8_t *dst = sym_out + ct * P::N1;
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r (in the staging buffer)
+      const uint4 *src = reinterpret_cast<const uint4 *>(pipe.stg) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      dst[j] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+    __syncwarp();  // r is consumed: the next v may land in the staging buffer
+    ct = nct;
+  }
+}
+
 
 // K4p: small batches with a warp PAIR per decryption (configs[0]: 1,024 decryptions are 7 per SM, and a
 // launch is the latency of one decryption: product ~10k cycles — the SM's shared memory saturated by its 7
@@ -1384,6 +1430,7 @@ struct DevInfo {
   int cap_decrypt_ws[6] = {0};  // resident CTAs/SM of k_decrypt_ws per level
   int cap_stage1[6] = {0};
   bool ready[6] = {false};
+  cudaMemPool_t pool = nullptr;  // the library's stream-ordered pool for K4x's symbol scratch
 };
 
 static std::mutex g_mu;
@@ -1400,13 +1447,14 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 // Which fused kernel a level uses (measured, profiles/r01/NOTES.md): 1 = one warp per ciphertext,
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
 // 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p),
-// 8 = compact lane-RS warps (K4l), 9 = K4l with static per-warp ranges. HQC_DEC_KERNEL=1..9 overrides.
+// 8 = compact lane-RS warps (K4l), 9 = K4l with static per-warp ranges, 10 = stages 1+2 and stage 3 as two
+// launches (K4x). HQC_DEC_KERNEL=1..10 overrides.
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 9 ? env : 0;
+  return env >= 1 && env <= 10 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1438,10 +1486,17 @@ template <class P> static size_t sb_max_batch(int sms) {
 // (17.7 vs 19.4 us: the SM's shared memory is saturated by the products either way and the pair's barriers
 // and idle second warp in stage 3 cost more than the halved stage 2; profiles/r02/ab_sp.log).
 template <class P> static size_t sp_max_batch(int sms) { return (size_t)env_long("HQC_SP_MAX", (long)sms * 4); }
+// K4x (two launches) for HQC-5 from ~96,000 (131,072: 4.77 vs 4.88 ms for K4a; 262,144 9.36 vs 9.58;
+// 4,194,304 in launches of 1,048,576: 2.83e7 vs 2.74e7/s; 65,536: 2.55 vs 2.53 — profiles/r02/ab_x5.log).
+template <class P> static size_t x_min_batch(int sms) {
+  const long v = env_long("HQC_X_MIN", P::level == 5 ? (long)sms * 640 : -1);
+  return v < 0 ? ~(size_t)0 : (size_t)v;
+}
 template <class P> static int dec_kernel_for(int sms, size_t batch) {
   if (dec_kernel_env()) return dec_kernel_env();
   if (batch <= sp_max_batch<P>(sms)) return 7;
-  return batch <= sb_max_batch<P>(sms) ? 5 : dec_kernel<P>();
+  if (batch <= sb_max_batch<P>(sms)) return 5;
+  return batch >= x_min_batch<P>(sms) ? 10 : dec_kernel<P>();
 }
 // The largest group (warps per CTA) of K4s whose shared memory fits one CTA.
 template <class P> constexpr uint32_t sb_max_g() {
@@ -1504,6 +1559,16 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
                                 SbSmem<P>::bytes(sb_max_g<P>()))) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * stage1_g<P>(), stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
+  if ((e = cudaFuncSetAttribute(k_decrypt_s12<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
+  if (!di.pool) {  // the library's own pool (the device's default pool and its release threshold stay the caller's)
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if ((e = cudaMemPoolCreate(&di.pool, &props)) != cudaSuccess) return e;
+    uint64_t keep = ~0ull;  // keep freed scratch for the next call instead of returning it at every sync
+    if ((e = cudaMemPoolSetAttribute(di.pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+  }
   di.ready[P::level] = true;
   return cudaSuccess;
 }
@@ -1554,6 +1619,15 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
     return;
   }
+  if (kind == 10) {  // k_decrypt_s12: one CTA of up to stage1_g warps per SM; *per = warps per CTA
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > stage1_g<P>()) g = stage1_g<P>();
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
+    return;
+  }
   if (kind == 6) {  // one CTA of up to MAX_G warps per SM; *per = warps per CTA
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
@@ -1592,8 +1666,20 @@ template <class P> static size_t dec_split() {
   const long s = env_long("HQC_DEC_SPLIT", -1);
   if (s >= 0) return (size_t)s;
   // measured at 4,194,304 (scripts/sweep_launch.py split, profiles/r02/sweep_split.log): HQC-1 +7% at 65,536
-  // per launch, HQC-5 +9% at 262,144; the HQC-3 warp pair is fastest unsplit
-  return P::level == 1 ? 65536u : P::level == 5 ? 262144u : 0u;
+  // per launch; HQC-5 K4a +9% at 262,144, K4x (its default there since) best at 1,048,576 (2.83e7/s against
+  // 2.81e7 unsplit and at 262,144; its symbol scratch is then 94 MB, profiles/r02/ab_x5.log); HQC-3 unsplit
+  return P::level == 1 ? 65536u : P::level == 5 ? 1048576u : 0u;
+}
+
+template <class P>
+static int launch_stage3_on(DevInfo *di, const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t batch, cudaStream_t st) {
+  const long ew = env_long("HQC_S3_WARPS", 4);  // experiments: warps per CTA (1..4)
+  const int warps = ew >= 1 && ew <= 4 ? (int)ew : 4;
+  size_t grid = (batch + 32 * warps - 1) / (32 * warps);
+  const size_t cap = (size_t)di->sms * 16;
+  if (grid > cap) grid = cap;
+  k_stage3<P><<<(unsigned)grid, 32 * warps, stage3_smem<P>(warps), st>>>(sym, m, ok, batch);
+  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
 }
 
 template <class P>
@@ -1627,6 +1713,17 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       k_decrypt_sb<P><<<grid, 32 * (unsigned)per, SbSmem<P>::bytes((uint32_t)per), st>>>(
           u, v, y, m, batch, (uint32_t)env_long("HQC_SB_STAGGER", 0));
       break;
+    case 10: {  // stages 1+2 -> symbols in a pool scratch -> stage 3 (stream-ordered: freed after k_stage3)
+      uint8_t *sym = nullptr;
+      if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&sym), batch * P::N1, di->pool, st) != cudaSuccess)
+        return HQC_ERR_CUDA;
+      k_decrypt_s12<P><<<grid, 32 * (unsigned)per, S1kSmem<P>::bytes((uint32_t)per), st>>>(
+          u, v, y, sym, batch, (uint32_t)env_long("HQC_S12_STAGGER", 0));
+      const int rc = launch_stage3_on<P>(di, sym, m, nullptr, batch, st);
+      const bool freed = cudaFreeAsync(sym, st) == cudaSuccess;
+      if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
+      break;
+    }
     default: k_decrypt_ws<P><<<grid, 128, decrypt_ws_smem<P>(), st>>>(u, v, y, m, batch, per); break;
   }
   return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
@@ -1680,6 +1777,8 @@ static int launch_stage1(const uint64_t *u, const uint32_t *y, const uint64_t *v
   size_t g = (batch + di->sms - 1) / (size_t)di->sms;  // warps per CTA: spread small batches over the SMs
   if (g < 1) g = 1;
   if (g > stage1_g<P>()) g = stage1_g<P>();
+  const long gmax = env_long("HQC_S1_G", 0);  // experiments: fewer warps per CTA
+  if (gmax > 0 && g > (size_t)gmax) g = (size_t)gmax;
   size_t grid = (batch + g - 1) / g;
   if (grid > (size_t)di->sms) grid = di->sms;
   k_stage1<P><<<(unsigned)grid, 32 * (unsigned)g, S1kSmem<P>::bytes((uint32_t)g), st>>>(u, y, v, r, batch);
@@ -1698,12 +1797,7 @@ static int launch_stage3(const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t bat
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
-  const int warps = 4;
-  size_t grid = (batch + 32 * warps - 1) / (32 * warps);
-  const size_t cap = (size_t)di->sms * 16;
-  if (grid > cap) grid = cap;
-  k_stage3<P><<<(unsigned)grid, 32 * warps, stage3_smem<P>(warps), st>>>(sym, m, ok, batch);
-  return cudaGetLastError() == cudaSuccess ? HQC_OK : HQC_ERR_CUDA;
+  return launch_stage3_on<P>(di, sym, m, ok, batch, st);
 }
 
 template <class P>
@@ -1771,10 +1865,21 @@ template <class P> static int kind_impl(size_t batch) {
   return dec_kernel_for<P>(di->sms, batch);
 }
 
-// How many kernel launches hqc_decrypt_batch makes for `batch` (the large-batch split, dec_split).
+// How many kernel launches hqc_decrypt_batch makes for `batch` (the large-batch split, dec_split; K4x is two
+// launches per part).
 template <class P> static long long nlaunch_impl(size_t batch) {
+  if (batch == 0) return 0;
+  DevInfo *di;
+  const int dev = cur_device(&di);
+  if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
   const size_t split = dec_split<P>();
-  return batch == 0 ? 0 : (split == 0 || batch <= split) ? 1 : (long long)((batch + split - 1) / split);
+  const size_t step = (split == 0 || batch <= split) ? batch : split;
+  long long n = 0;
+  for (size_t off = 0; off < batch; off += step) {
+    const size_t c = batch - off < step ? batch - off : step;
+    n += dec_kernel_for<P>(di->sms, c) == 10 ? 2 : 1;
+  }
+  return n;
 }
 
 template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
@@ -1785,7 +1890,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
   *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
-        : (kind == 5 || kind == 6 || kind == 8 || kind == 9) ? (int)per : kind == 7 ? 2 * (int)per : 4;
+        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10) ? (int)per : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

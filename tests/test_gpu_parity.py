@@ -267,12 +267,11 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9", "10"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
-    """The library picks the warp-pair kernel (HQC-3) or the one-warp kernel (HQC-1/5) per level, and the
-    small-batch group kernel (5) for small batches; the warp-specialised kernel (3) and the
-    tensor-memory-product kernel (4) are alternatives. HQC_DEC_KERNEL
-    forces each (read once per process), so each runs in a subprocess on every level."""
+    """Every decrypt kernel (hqc.KERNEL_NAMES; the library picks one per level and batch)
+    against the oracle on every level, including 10, the two-launch split with its pool scratch.
+    HQC_DEC_KERNEL forces each (read once per process), so each runs in a subprocess."""
     import subprocess
     import sys
     import os
@@ -297,6 +296,53 @@ print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, HQC_DEC_KERNEL=kernel)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_two_launch_kernel_ragged_split_and_graph_capture():
+    """Kernel 10 (k_decrypt_s12 + k_stage3, HQC-5's large-batch default) takes its symbol scratch from the
+    library's stream-ordered pool: split into ragged parts (HQC_DEC_SPLIT=1000 over 2,500 rows: 1000,
+    1000, 500) it matches the oracle, and the call captured in a CUDA graph (pool allocation inside the
+    capture) replays to the same outputs; a mixed-level call after it is unaffected."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, "tests")
+import oracle
+from paper_2512_12904_b200 import hqc
+from workloads import valid_batch
+d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
+for level in (5, 1):
+    W = valid_batch(level, 90000, 2500, 41)
+    p = hqc.params(level)
+    assert hqc.hqc_decrypt_launch_kernel(level, 2500) == 10
+    assert hqc.hqc_decrypt_launch_count(level, 2500) == 6
+    u, v, y = d(W["u"]), d(W["v"]), d(W["y"])
+    ref = oracle.decrypt_batch(W["params"], W["u"], W["v"], W["y"])
+    m = torch.zeros(2500 * p.k, dtype=torch.uint8, device="cuda")
+    hqc.hqc_decrypt_batch(level, u, v, y, m)
+    torch.cuda.synchronize()
+    assert (m.cpu().numpy().reshape(2500, p.k) == ref).all(), level
+    m.zero_()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            hqc.hqc_decrypt_batch(level, u, v, y, m, stream=s)
+    for _ in range(2):
+        m.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert (m.cpu().numpy().reshape(2500, p.k) == ref).all(), ("graph", level)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HQC_DEC_KERNEL="10", HQC_DEC_SPLIT="1000")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
