@@ -1,0 +1,13 @@
+# ncu evidence for K4x (HQC-5 two launches) and the current k_encrypt2 (one capture each, after a plain run)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+run() {  # name, kernel regex, command...
+  local name=$1 rx=$2; shift 2
+  timeout 300 "$@" > gpurun_out/r3_plain_$name.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$rx -s 2 -c 1 -o gpurun_out/r3_$name "$@" > gpurun_out/r3_ncu_$name.log 2>&1
+  echo "$name exit $?" >> gpurun_out/r3_status.log
+}
+run x12_L5 k_decrypt_s12 python scripts/time_kind.py 5:262144
+run x3_L5 k_stage3 python scripts/time_kind.py 5:262144
+run enc_L1 k_encrypt2 python scripts/time_encrypt.py 1
+run enc_L3 k_encrypt2 python scripts/time_encrypt.py 3
