@@ -180,10 +180,12 @@ __device__ __forceinline__ void s1_stage_d(const uint32_t *sy, uint32_t *dsm, in
 // not by the data). acc[k] accumulates output word lane*R + k.
 template <class P, class S>
 __device__ __forceinline__ void s1_product_range(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[S::R],
-                                                 int lane, uint32_t j0, uint32_t j1) {
+                                                 int lane, uint32_t j0, uint32_t j1, bool init = true) {
   constexpr int R = S::R;
+  if (init) {
 #pragma unroll
-  for (int k = 0; k < R; k++) acc[k] = 0;
+    for (int k = 0; k < R; k++) acc[k] = 0;
+  }
   const uint32_t *Eb = E + lane * R;
   uint32_t j = j0;
   constexpr int kUnroll = s1_unroll<P>();
