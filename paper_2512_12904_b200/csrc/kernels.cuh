@@ -765,46 +765,6 @@ template <class P> struct SbPipe {
   }
 };
 
-// SbPipe::run for a product warp of K4y (below): the v row is requested only after the first half of the
-// support indices, once the decoder warp has released the staging buffer (empty_bar, parity of the
-// previous item) — it still lands long before the product ends.
-template <class P>
-__device__ __forceinline__ void sb_run_w(SbPipe<P> &pp, size_t ct, bool has_next, size_t next, int lane,
-                                         uint64_t *empty_bar, uint32_t nitems) {
-  using ST = DecShapeT<P>;
-  using M = SbPipeSmem<P>;
-  constexpr uint32_t TW = dec_tail_words<P>();
-  constexpr uint32_t JH = (ST::WT / 2) & ~1u;  // even split point of the support
-  mbar_wait(pp.bar, pp.ph_uy);
-  pp.ph_uy ^= 1u;
-  s1_stage_d<P, DecShape<P>>(pp.stg_y, pp.dsm, lane);
-  pp.build_E(lane);
-  __syncwarp();
-  uint32_t acc[ST::R];
-  s1_product_range<P, ST>(pp.E, pp.dsm, acc, lane, 0, JH, true);
-  if (nitems > 0) mbar_wait(empty_bar, (nitems - 1) & 1u);  // the previous r has been decoded
-  if (lane == 0) {
-    fence_proxy_async_smem();
-    mbar_expect_tx(pp.bar + 1, M::VB);
-    tma_load_1d(pp.stg, pp.v + ct * P::V_WORDS, M::VB, pp.bar + 1);
-  }
-  s1_product_range<P, ST>(pp.E, pp.dsm, acc, lane, JH, ST::WT, false);
-  uint32_t mine = 0;
-  if constexpr (TW > 0) {
-    uint32_t t[TW];
-    s1_tail_words<P, ST, ST::NOUT, TW>(pp.E, pp.dsm, lane, t);
-#pragma unroll
-    for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
-  }
-  __syncwarp();  // E, dsm and stg_y are read: the next rows may land
-  if (has_next) pp.issue_uy(next, lane);
-  mbar_wait(pp.bar + 1, pp.ph_v);
-  pp.ph_v ^= 1u;
-  s1_store_r_xor<ST>(acc, pp.stg, pp.stg, lane);
-  if (TW > 0 && (uint32_t)lane < TW) pp.stg[ST::NOUT + lane] = mine ^ pp.stg[ST::NOUT + lane];
-  __syncwarp();
-}
-
 template <class P> struct SbSmem {
   static constexpr uint32_t MAX_G = 16;  // warps per CTA; 512 threads: <= 128 registers
   static constexpr uint32_t SYM_BYTES = round_up(P::N1, 16);  // the warp's received symbols
@@ -918,99 +878,6 @@ __global__ void __launch_bounds__(512, 1) k_decrypt_s12(const uint64_t *__restri
     }
     __syncwarp();  // r is consumed: the next v may land in the staging buffer
     ct = nct;
-  }
-}
-
-
-// K4y (round 2, experiment for HQC-5): K4x's first launch with the roles split. G product warps run
-// stage 1 on the SbPipe and leave r in their staging buffers; NRM decoder warps run stage 2 on whichever
-// staging buffer is ready (per-slot "full" / "empty" mbarriers, polled with test_wait) and write the
-// symbols; stage 2 no longer stalls the products that feed the shared-memory pipe.
-template <class P> struct XwSmem {
-  static constexpr uint32_t SLOT = 32;  // full mbarrier, empty mbarrier, ct
-  static constexpr uint32_t bytes(uint32_t g) { return 16 + g * (SLOT + SbPipeSmem<P>::BYTES); }
-  static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
-};
-template <class P>
-__global__ void __launch_bounds__(512, 1) k_decrypt_s12w(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
-                                                         const uint32_t *__restrict__ y, uint8_t *__restrict__ sym_out,
-                                                         size_t batch, uint32_t G) {
-  using M = XwSmem<P>;
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t NRM = (blockDim.x >> 5) - G;
-  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem);
-  uint8_t *slots = smem + 16;
-  uint8_t *pipes = smem + 16 + G * M::SLOT;
-  auto full = [&](uint32_t s) { return reinterpret_cast<uint64_t *>(slots + s * M::SLOT); };
-  auto empty = [&](uint32_t s) { return reinterpret_cast<uint64_t *>(slots + s * M::SLOT + 8); };
-  auto slot_ct = [&](uint32_t s) { return reinterpret_cast<volatile unsigned long long *>(slots + s * M::SLOT + 16); };
-  if (threadIdx.x < G) {
-    mbar_init(full(threadIdx.x), 32);  // every lane of the product warp arrives
-    mbar_init(empty(threadIdx.x), 32);  // every lane of the decoder warp arrives
-  }
-  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
-  const size_t c0 = (size_t)blockIdx.x * per_cta;
-  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
-  if ((uint32_t)wib < G) {
-    SbPipe<P> pipe(pipes + (size_t)wib * SbPipeSmem<P>::BYTES, u, v, y, lane);
-    size_t ct = c0 + wib;
-    if (ct < c1) pipe.issue_uy(ct, lane);
-    if (threadIdx.x == 0) *next_item = G;
-    __syncthreads();
-    uint32_t nitems = 0;
-    while (ct < c1) {
-      uint32_t nx = 0;
-      if (lane == 0) nx = atomicAdd(next_item, 1u);
-      const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
-      sb_run_w<P>(pipe, ct, nct < c1, nct, lane, empty(wib), nitems);
-      if (lane == 0) *slot_ct(wib) = ct;
-      __syncwarp();
-      mbar_arrive(full(wib));  // r (in stg) and ct are published
-      nitems++;
-      ct = nct;
-    }
-    if (nitems > 0) mbar_wait(empty(wib), (nitems - 1) & 1u);
-    if (lane == 0) *slot_ct(wib) = ~0ull;  // no more items in this slot
-    __syncwarp();
-    mbar_arrive(full(wib));
-  } else {
-    __syncthreads();
-    const uint32_t k = wib - G;
-    uint32_t ph = 0, done = 0, mine = 0;
-    for (uint32_t s = k; s < G; s += NRM) mine |= 1u << s;
-    while (done != mine) {
-      bool got = false;
-      for (uint32_t s = k; s < G; s += NRM) {
-        if ((done >> s) & 1u) continue;
-        const bool ready = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)mbar_test(full(s), (ph >> s) & 1u) : 0u, 0) != 0;
-        if (!ready) continue;
-        mbar_wait(full(s), (ph >> s) & 1u);  // every lane acquires the published r
-        ph ^= 1u << s;
-        const unsigned long long cts = *slot_ct(s);
-        if (cts == ~0ull) {
-          done |= 1u << s;
-          continue;
-        }
-        const uint32_t *stg = reinterpret_cast<const uint32_t *>(pipes + (size_t)s * SbPipeSmem<P>::BYTES +
-                                                                 SbPipeSmem<P>::E_BYTES);
-        uint8_t *dst = sym_out + (size_t)cts * P::N1;
-        for (uint32_t j = lane; j < P::N1; j += 32) {
-          const uint4 *src = reinterpret_cast<const uint4 *>(stg) + j * (P::N2 / 128);
-          uint32_t X[P::MULT * 4];
-#pragma unroll
-          for (int c = 0; c < (int)P::MULT; c++) {
-            const uint4 x = src[c];
-            X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
-          }
-          dst[j] = (uint8_t)rm_decode_block<P::MULT>(X);
-        }
-        __syncwarp();
-        mbar_arrive(empty(s));  // the staging buffer may take the next v
-        got = true;
-      }
-      if (!got) __nanosleep(256);
-    }
   }
 }
 
@@ -1587,7 +1454,7 @@ static int dec_kernel_env() {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 11 ? env : 0;
+  return env >= 1 && env <= 10 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1654,18 +1521,6 @@ template <class P> static int stage1_kernel() {
   return 1;
 }
 template <class P> static uint32_t stage1_g() { return S1kSmem<P>::fit(16); }
-// K4y: decoder warps per CTA (HQC_X_RM, 1..4) and product warps (what shared memory holds beside them)
-static uint32_t x_w_rm() {
-  const long r = env_long("HQC_X_RM", 2);
-  return r >= 1 && r <= 4 ? (uint32_t)r : 2u;
-}
-template <class P> static uint32_t x_w_g() {
-  uint32_t g = XwSmem<P>::fit(16 - x_w_rm());
-  const long gmax = env_long("HQC_S1_G", 0);
-  if (gmax > 0 && g > (uint32_t)gmax) g = (uint32_t)gmax;
-  return g;
-}
-template <class P> static uint32_t stage1_smem() { return S1kSmem<P>::bytes(stage1_g<P>()); }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }
@@ -1704,8 +1559,6 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * stage1_g<P>(), stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   if ((e = cudaFuncSetAttribute(k_decrypt_s12<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_decrypt_s12w<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                XwSmem<P>::bytes(XwSmem<P>::fit(15)))) != cudaSuccess) return e;
   if (!di.pool) {  // the library's own pool (the device's default pool and its release threshold stay the caller's)
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
@@ -1760,15 +1613,6 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > WlSmem<P>::MAX_G) g = WlSmem<P>::MAX_G;
-    *per = g;
-    const size_t groups = (batch + g - 1) / g;
-    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
-    return;
-  }
-  if (kind == 11) {  // k_decrypt_s12w: G product warps (+ decoder warps); *per = G
-    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
-    if (g < 1) g = 1;
-    if (g > x_w_g<P>()) g = x_w_g<P>();
     *per = g;
     const size_t groups = (batch + g - 1) / g;
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
@@ -1874,17 +1718,6 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
         return HQC_ERR_CUDA;
       k_decrypt_s12<P><<<grid, 32 * (unsigned)per, S1kSmem<P>::bytes((uint32_t)per), st>>>(
           u, v, y, sym, batch, (uint32_t)env_long("HQC_S12_STAGGER", 0));
-      const int rc = launch_stage3_on<P>(di, sym, m, nullptr, batch, st);
-      const bool freed = cudaFreeAsync(sym, st) == cudaSuccess;
-      if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
-      break;
-    }
-    case 11: {  // K4y: as K4x with the first launch's roles split
-      uint8_t *sym = nullptr;
-      if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&sym), batch * P::N1, di->pool, st) != cudaSuccess)
-        return HQC_ERR_CUDA;
-      const uint32_t g = (uint32_t)per, nw = g + x_w_rm();
-      k_decrypt_s12w<P><<<grid, 32 * nw, XwSmem<P>::bytes(g), st>>>(u, v, y, sym, batch, g);
       const int rc = launch_stage3_on<P>(di, sym, m, nullptr, batch, st);
       const bool freed = cudaFreeAsync(sym, st) == cudaSuccess;
       if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
@@ -2043,8 +1876,7 @@ template <class P> static long long nlaunch_impl(size_t batch) {
   long long n = 0;
   for (size_t off = 0; off < batch; off += step) {
     const size_t c = batch - off < step ? batch - off : step;
-    const int kd = dec_kernel_for<P>(di->sms, c);
-    n += (kd == 10 || kd == 11) ? 2 : 1;
+    n += dec_kernel_for<P>(di->sms, c) == 10 ? 2 : 1;
   }
   return n;
 }
@@ -2057,7 +1889,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
   *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
-        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10) ? (int)per : kind == 11 ? (int)(per + x_w_rm()) : kind == 7 ? 2 * (int)per : 4;
+        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10) ? (int)per : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

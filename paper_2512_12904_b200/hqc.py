@@ -239,8 +239,7 @@ KERNEL_NAMES = {1: "k_decrypt_w1 (fused, one warp per ciphertext range, lane-per
                 7: "k_decrypt_sp (fused, warp pair per ciphertext, small batches)",
                 8: "k_decrypt_wl (fused, compact warps: v above u in E, chunks of 32, lane-per-word RS)",
                 9: "k_decrypt_wl<static> (fused, compact warps, per-warp contiguous ranges)",
-                10: "k_decrypt_s12 + k_stage3 (stages 1+2, symbols via HBM, lane-per-word RS: two launches)",
-                11: "k_decrypt_s12w + k_stage3 (as 10, product and stage-2 warps specialised)"}
+                10: "k_decrypt_s12 + k_stage3 (stages 1+2, symbols via HBM, lane-per-word RS: two launches)"}
 
 
 def hqc_decrypt_launch_kernel(level: int, batch: int) -> int:
