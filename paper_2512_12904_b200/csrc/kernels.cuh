@@ -1521,6 +1521,7 @@ template <class P> static int stage1_kernel() {
   return 1;
 }
 template <class P> static uint32_t stage1_g() { return S1kSmem<P>::fit(16); }
+template <class P> static uint32_t stage1_smem() { return S1kSmem<P>::bytes(stage1_g<P>()); }
 template <class P> static uint32_t stage3_smem(int warps) {
   return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }
