@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libhqcgpu.so")
 SOURCES = ["hqc_gpu.cu", "hqc_l1.cu", "hqc_l3.cu", "hqc_l5.cu"]
-DEPS = SOURCES + ["kernels.cuh", "launchers.h", "levels.cuh", "async_copy.cuh", "encrypt.cuh", "gf256.cuh", "stage1.cuh", "stage1_tmem.cuh", "stage2.cuh", "stage3.cuh", "keccak.cuh", "kem.cuh", "syndromes.cuh", "exp_timing.cuh", "stage3_warp.cuh"]
+DEPS = SOURCES + ["kernels.cuh", "launchers.h", "levels.cuh", "async_copy.cuh", "encrypt.cuh", "gf256.cuh", "stage1.cuh", "seg_plans.cuh", "stage1_tmem.cuh", "stage2.cuh", "stage3.cuh", "keccak.cuh", "kem.cuh", "syndromes.cuh", "exp_timing.cuh", "stage3_warp.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

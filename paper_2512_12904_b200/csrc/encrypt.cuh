@@ -200,6 +200,21 @@ __device__ __forceinline__ void warp_product(uint32_t *su, const uint32_t *ssup,
   __syncwarp();
 }
 
+// The same with the segmented layout (stage1.cuh: s1_seg_product); S sizes E, G is the product's SegShape.
+template <class P, class S, class G>
+__device__ __forceinline__ void warp_product_seg(uint32_t *su, const uint32_t *ssup, uint32_t *E, uint32_t *dsm,
+                                                 int lane) {
+  static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+  s1_stage_d<P, S>(ssup, dsm, lane);
+  s1_build_E<P, S>(su, E, lane);
+  __syncwarp();
+  uint32_t acc[G::LMAX], top;
+  s1_seg_product<P, G>(E, dsm, acc, top, lane);
+  __syncwarp();
+  s1_seg_store<G>(acc, top, E, lane);
+  __syncwarp();
+}
+
 // XOR the bits of a support (first wt entries, positions < limit) into a bit vector in smem.
 __device__ __forceinline__ void xor_support_bits(uint32_t *vec, const uint32_t *supp, uint32_t wt, uint32_t limit,
                                                  int lane) {
@@ -238,7 +253,11 @@ __global__ void __launch_bounds__(32) k_keygen(const uint64_t *__restrict__ h, c
     copy_g2s(sx, x + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     copy_g2s(sy, y + kk * P::Y_STRIDE, P::Y_STRIDE, lane);
     __syncwarp();
+#if HQC_S1_SEG
+    warp_product_seg<P, KeyShape<P>, KeySeg<P>>(stg, sy, E, dsm, lane);
+#else
     warp_product<P, S, enc_tail<P>()>(stg, sy, E, dsm, lane);
+#endif
     xor_support_bits(E, sx, P::W, P::N, lane);
     __syncwarp();
     if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;  // bits >= n are zero
@@ -283,7 +302,11 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
     for (uint32_t j = lane; j < P::K; j += 32) msg[j] = m[ct * P::K + j];
     __syncwarp();
     // u = r1 + h * r2 (all n bits)
+#if HQC_S1_SEG
+    warp_product_seg<P, FullShape<P>, FullSeg<P>>(stg, s_r2, E, dsm, lane);
+#else
     warp_product<P, FullShape<P>>(stg, s_r2, E, dsm, lane);
+#endif
     xor_support_bits(E, s_r1, P::WR, P::N, lane);
     __syncwarp();
     if (lane == 0) E[P::Q0] &= (1u << P::C) - 1u;
@@ -304,7 +327,11 @@ __global__ void __launch_bounds__(32) k_encrypt(const uint64_t *__restrict__ h, 
     copy_g2s(stg, s + key * P::U_STRIDE, 2 * P::U_STRIDE, lane);
     rs_encode_warp<P>(msg, cw, lane);
     __syncwarp();
+#if HQC_S1_SEG
+    warp_product_seg<P, EncVShape<P>, EncVSeg<P>>(stg, s_r2, E, dsm, lane);
+#else
     warp_product<P, EncVShape<P>>(stg, s_r2, E, dsm, lane);
+#endif
     for (uint32_t j = lane; j < P::N1; j += 32) {  // RM-encode symbol j into block j, every copy
       uint32_t w[4];
       rm_encode_byte(cw[j], w);
@@ -467,6 +494,14 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
       using S = typename M::SU;
       s1_stage_d<P, S>(s_r2, dsm, lane);
       __syncwarp();
+#if HQC_S1_SEG
+      using G = FullSeg<P>;
+      static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+      uint32_t acc[G::LMAX], top;
+      s1_seg_product<P, G>(E, dsm, acc, top, lane);
+      out_free();
+      s1_seg_store<G>(acc, top, out, lane);
+#else
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
       out_free();
@@ -476,6 +511,7 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
         s1_tail_words<P, S, S::NOUT, enc_tail<P>()>(E, dsm, lane, t);
         store_tail<S, enc_tail<P>()>(t, out, lane);
       }
+#endif
       __syncwarp();
       xor_support_bits(out, s_x, P::WR, P::N, lane);
       __syncwarp();
@@ -498,6 +534,14 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
       rs_encode_warp_log<P>(msg, cw, gf8, lane);
       s1_stage_d<P, S>(s_r2, dsm, lane);
       __syncwarp();
+#if HQC_S1_SEG
+      using G = EncVSeg<P>;
+      static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+      uint32_t acc[G::LMAX], top;
+      s1_seg_product<P, G>(E, dsm, acc, top, lane);
+      out_free();
+      s1_seg_store<G>(acc, top, out, lane);
+#else
       uint32_t acc[S::R];
       s1_product<P, S>(E, dsm, acc, lane);
       out_free();
@@ -507,6 +551,7 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
         s1_tail_words<P, S, S::NOUT, enc_tail_v<P>()>(E, dsm, lane, t);
         store_tail<S, enc_tail_v<P>()>(t, out, lane);
       }
+#endif
       __syncwarp();
       for (uint32_t j = lane; j < P::N1; j += 32) {  // RM-encode symbol j into block j, every copy
         uint32_t w[4];

@@ -136,6 +136,20 @@ template <class P> struct S1Pipe {
     PHASE(2);
     if (v) issue_v(ct, lane);
     else if (has_next) issue_uy(next, lane);  // no v to stage: the next rows land during this product
+#if HQC_S1_SEG && !HQC_S1_SHFL
+    using G = DecSeg<P>;
+    static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    __syncwarp();  // every lane is done reading E: r overwrites it
+    PHASE(3);
+    if (v) {
+      wait();  // v has landed in the staging buffer during the product loop
+      s1_seg_store_xor<G>(acc, top, rout, stg_u, lane);
+    } else {
+      s1_seg_store<G>(acc, top, rout, lane);
+    }
+#else
     uint32_t acc[ST::R];
 #if HQC_S1_SHFL
     s1_product_range_sh<P, ST>(E, dsm, acc, lane, 0, P::W);
@@ -167,6 +181,7 @@ template <class P> struct S1Pipe {
 #endif
       if (TW > 0 && (uint32_t)lane < TW) rout[ST::NOUT + lane] = mine;
     }
+#endif
     __syncwarp();
     PHASE(4);
     if (v && has_next) issue_uy(next, lane);
@@ -616,6 +631,12 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     s1_stage_d<P, S>(stg_y, dsm, lane);
     s1_build_E_upper<P, S>(E, lane);  // the shifted upper copy of E from u's row in its lower half
     __syncwarp();
+#if HQC_S1_SEG
+    using G = DecSeg<P>;
+    static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+#else
     uint32_t acc[ST::R];
     s1_product<P, ST>(E, dsm, acc, lane);
     uint32_t mine = 0;
@@ -625,6 +646,7 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
 #pragma unroll
       for (uint32_t i = 0; i < TW; i++) mine = (uint32_t)lane == i ? t[i] : mine;
     }
+#endif
     __syncwarp();  // E is read: v may land above u's row, the next u in it
     if (lane == 0) {
       fence_proxy_async_smem();
@@ -635,8 +657,12 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     if (lane == 0) cidx[slot] = (uint32_t)(ct - cbase);
     mbar_wait(bar + 1, ph_v);
     ph_v ^= 1u;
+#if HQC_S1_SEG
+    s1_seg_store_xor<G>(acc, top, Rv, Rv, lane);  // r = acc ^ v in place
+#else
     s1_store_r_xor<ST>(acc, Rv, Rv, lane);  // r = acc ^ v in place
     if (TW > 0 && (uint32_t)lane < TW) Rv[ST::NOUT + lane] = mine ^ Rv[ST::NOUT + lane];
+#endif
     __syncwarp();
     for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2 into the chunk's slot
       const uint4 *src = reinterpret_cast<const uint4 *>(Rv) + j * (P::N2 / 128);
@@ -739,6 +765,22 @@ template <class P> struct SbPipe {
       mbar_expect_tx(bar + 1, M::VB);
       tma_load_1d(stg, v + ct * P::V_WORDS, M::VB, bar + 1);
     }
+#if HQC_S1_SEG
+    using G = DecSeg<P>;
+    static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    __syncwarp();  // every lane is done reading E (and dsm, stg_y): the next rows may land
+    PHASE(3);
+    if (has_next) issue_uy(next, lane);
+    if (v) {
+      mbar_wait(bar + 1, ph_v);
+      ph_v ^= 1u;
+      s1_seg_store_xor<G>(acc, top, stg, stg, lane);  // r = acc ^ v in place (each lane its own words)
+    } else {  // the standalone product: r = acc
+      s1_seg_store<G>(acc, top, stg, lane);
+    }
+#else
     uint32_t acc[ST::R];
     s1_product<P, ST>(E, dsm, acc, lane);
     uint32_t mine = 0;  // lane i < TW: word ST::NOUT + i
@@ -760,6 +802,7 @@ template <class P> struct SbPipe {
       s1_store_r<ST>(acc, stg, lane);
       if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine;
     }
+#endif
     __syncwarp();
     PHASE(4);
   }
@@ -962,6 +1005,19 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
     }
     ph_uy ^= 1u;
     pair_sync(bid);  // E and the rotation amounts are ready
+#if HQC_S1_SEG
+    using G = DecSeg<P>;
+    static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G>(E, dsm, acc, top, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
+    if (wa) s1_seg_store<G>(acc, top, X, lane);
+    pair_sync(bid);  // both warps are done with E; B's image is in X
+    if (wa == 0) {
+      if (has_next && lane == 0) issue_uy(ct + step);
+      mbar_wait(bar + 1, ph_v);
+      s1_seg_store_xor2<G>(acc, top, stg, X, stg, lane);  // r = acc_A ^ acc_B ^ v, in place over v
+    }
+#else
     uint32_t acc[ST::R];
     s1_product_range<P, ST>(E, dsm, acc, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
     uint32_t mine = 0;
@@ -981,6 +1037,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
       s1_store_r_xor2<ST>(acc, stg, X, stg, lane);  // r = acc_A ^ acc_B ^ v, in place over v
       if (TW > 0 && (uint32_t)lane < TW) stg[ST::NOUT + lane] = mine ^ stg[ST::NOUT + lane];
     }
+#endif
     ph_v ^= 1u;
     pair_sync(bid);  // r complete
     constexpr uint32_t NH = (P::N1 + 1) / 2;  // stage 2: A blocks [0, NH), B [NH, n1)

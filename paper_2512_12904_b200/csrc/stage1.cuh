@@ -16,8 +16,15 @@
 #include <cstdint>
 
 #include "levels.cuh"
+#include "seg_plans.cuh"
 
 namespace hqc {
+
+// The segmented lane layout of the product (s1_seg_product, below) in the default kernels; 0 restores the
+// round-2 R-word lanes with s1_tail_words (an experiment switch, A/B in profiles/r02/ab_seg.log).
+#ifndef HQC_S1_SEG
+#define HQC_S1_SEG 1
+#endif
 
 // index-pair loop unroll per level, from scripts/exp_unroll.py (2: -0.5% HQC-1/3; 3: -2.4% HQC-5)
 template <class P> constexpr int s1_unroll() {
@@ -399,6 +406,205 @@ __device__ __forceinline__ void s1_xor_v(uint32_t *rsm, const uint32_t *sv, int 
     rr.x ^= vv.x; rr.y ^= vv.y; rr.z ^= vv.z; rr.w ^= vv.w;
     reinterpret_cast<uint4 *>(rsm)[c] = rr;
   }
+}
+
+// ------------------------------------------------------------------------------------------------
+// The SEGMENTED lane layout (round 2). The R-word lanes above load R + 1 window words per
+// (index, lane) for R outputs — the (R+1)-th only for the high part of the lane's last funnel — and R is
+// odd (conflict-free strides), so a warp issues R + 1 = ceil(NOUT/32) + 1..2 loads per index plus, where
+// 32 R < NOUT, a ragged top (s1_tail_words: lane-per-index loads with random banks). Here:
+//  * lane L owns the output words [st_L, st_L + len_L), contiguous in lane order, len_L in [LMIN, LMAX]
+//    (LMAX = ceil(NB/32)), the starts st_L DISTINCT mod 32 (seg_plans.cuh, generated by
+//    scripts/gen_segments.py), so the lanes' loads E[o + st_L + k] of every slot k hit 32 distinct banks;
+//  * a funnel splits into two shifts that do not overlap: SHF(lo, hi, s) = SHF(lo, 0, s) ^ SHF(0, hi, s).
+//    A LONG lane (len_L = LMAX) loads only its own LMAX words; the high part of its last funnel comes from
+//    its right neighbour, which accumulates SHF(0, first word, s) over the indices in one register (`pre`)
+//    and passes it on with ONE shuffle per product (round 2's per-index SHFL variant lost: it shares the
+//    shared-memory data path). A SHORT lane loads its len_L + 1 words itself, in slots the long lanes use;
+//  * the top neighbour word(s) of a long last lane, E[o + NB .. o + NOUT], come from a lane-per-index pass
+//    (TP words per index, one REDUX per word) — HQC-3 (1,120 = 32 x 35 words) and HQC-5.
+// So a warp issues LMAX loads per index (HQC-1 18, HQC-3 35, HQC-5 57; round 2: 18 + a 9-word tail, 36, 58)
+// for 1.5 (LMAX + 1) ALU ops per index (the extra shift pair of `pre`). The loop count is the level's w for
+// every ciphertext; the slot predicates depend on the lane only.
+template <class P, uint32_t NOUT_, uint32_t WT_> struct SegShape {
+  using PL = SegPlan<NOUT_>;
+  static constexpr uint32_t NOUT = NOUT_, WT = WT_, WPAD = round_up(WT_, 4);
+  static constexpr uint32_t NB = PL::NB, LMAX = PL::LMAX, TP = PL::TP;
+  static constexpr uint32_t lmin() {
+    uint32_t m = LMAX;
+    for (int i = 0; i < 32; i++) m = PL::LEN[i] < m ? PL::LEN[i] : m;
+    return m;
+  }
+  static constexpr uint32_t LMIN = lmin();
+  static constexpr uint32_t def_mask(int bit) {
+    uint32_t m = 0;
+    for (int i = 0; i < 32; i++) m |= (((LMAX - PL::LEN[i]) >> bit) & 1u) << i;
+    return m;
+  }
+  static constexpr uint32_t D1 = def_mask(0), D2 = def_mask(1);  // bits of LMAX - len_L
+  static constexpr bool valid() {
+    uint32_t st = 0, seen = 0;
+    for (int i = 0; i < 32; i++) {
+      if (PL::LEN[i] > LMAX || LMAX - PL::LEN[i] > 3) return false;
+      if ((seen >> (st & 31)) & 1u) return false;  // two starts in one bank
+      seen |= 1u << (st & 31);
+      st += PL::LEN[i];
+    }
+    if (st != NB) return false;
+    if (TP == 0) return NB == NOUT && PL::LEN[31] < LMAX;  // the last lane loads its own neighbour word
+    return NB + TP - 1 == NOUT && PL::LEN[31] == LMAX && TP <= 2;
+  }
+  static_assert(valid(), "seg_plans.cuh: lengths, distinct starts mod 32, top handling");
+  // E must hold the window words up to o + NOUT, o <= Q0 (every d <= n)
+  static constexpr uint32_t E_NEED = P::Q0 + NOUT + 1;
+  __device__ __forceinline__ static uint32_t len(int lane) {
+    return LMAX - ((D1 >> lane) & 1u) - 2u * ((D2 >> lane) & 1u);
+  }
+  __device__ __forceinline__ static uint32_t start(int lane) {
+    const uint32_t lt = (1u << lane) - 1u;
+    return (uint32_t)lane * LMAX - __popc(D1 & lt) - 2u * __popc(D2 & lt);
+  }
+};
+template <class P> using DecSeg = SegShape<P, P::NW, P::W>;        // u*y truncated (decrypt r)
+template <class P> using FullSeg = SegShape<P, P::Q0 + 1, P::WR>;  // h*r2, all n bits (Encrypt u)
+template <class P> using KeySeg = SegShape<P, P::Q0 + 1, P::W>;    // h*y (KeyGen s)
+template <class P> using EncVSeg = SegShape<P, P::NW, P::WR>;      // s*r2 truncated (Encrypt v)
+
+// The product over support indices [j0, j1) (j0 even) in the segmented layout: acc[k] = output word
+// st_L + k for k < len_L (complete, the neighbour's part included); `top` = word NB + lane for lane < TP - 1.
+template <class P, class G>
+__device__ __forceinline__ void s1_seg_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[G::LMAX],
+                                               uint32_t &top, int lane, uint32_t j0 = 0, uint32_t j1 = G::WT) {
+  constexpr int L = (int)G::LMAX, LMIN = (int)G::LMIN;
+  constexpr int NPS = L - 1 - LMIN > 0 ? L - 1 - LMIN : 1;  // predicated slots k + 1 in (LMIN, L - 1]
+  const uint32_t len = G::len(lane);
+  const uint32_t *Eb = E + G::start(lane);
+#pragma unroll
+  for (int k = 0; k < L; k++) acc[k] = 0;
+  uint32_t pre = 0;
+  // Slots above LMIN are loaded only by lanes whose segment reaches them; the others keep a stale value
+  // (loop-carried registers, no zeroing): it reaches only accumulators above their segment, never stored.
+  uint32_t ja[NPS], jb[NPS];
+#pragma unroll
+  for (int i = 0; i < NPS; i++) ja[i] = jb[i] = 0;
+  uint32_t j = j0;
+  constexpr int kUnroll = s1_unroll<P>();
+#pragma unroll kUnroll
+  for (; j + 1 < j1; j += 2) {
+    const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
+    const uint32_t *p0 = s1_window<P>(Eb, dd.x);
+    const uint32_t *p1 = s1_window<P>(Eb, dd.y);
+    uint32_t a0 = p0[0], b0 = p1[0];
+    pre ^= __funnelshift_r(0u, a0, dd.x) ^ __funnelshift_r(0u, b0, dd.y);
+#pragma unroll
+    for (int k = 0; k < L; k++) {
+      uint32_t a1, b1;
+      if (k + 1 == L) {
+        a1 = 0u;
+        b1 = 0u;
+      } else if (k + 1 <= LMIN) {
+        a1 = p0[k + 1];
+        b1 = p1[k + 1];
+      } else {
+        const int i = k - LMIN;
+        if ((uint32_t)(k + 1) <= len) {
+          ja[i] = p0[k + 1];
+          jb[i] = p1[k + 1];
+        }
+        a1 = ja[i];
+        b1 = jb[i];
+      }
+      acc[k] ^= __funnelshift_r(a0, a1, dd.x) ^ __funnelshift_r(b0, b1, dd.y);
+      a0 = a1;
+      b0 = b1;
+    }
+  }
+  if (j < j1) {
+    const uint32_t d = dsm[j];
+    const uint32_t *p0 = s1_window<P>(Eb, d);
+    uint32_t a0 = p0[0];
+    pre ^= __funnelshift_r(0u, a0, d);
+#pragma unroll
+    for (int k = 0; k < L; k++) {
+      uint32_t a1;
+      if (k + 1 == L) {
+        a1 = 0u;
+      } else if (k + 1 <= LMIN) {
+        a1 = p0[k + 1];
+      } else {
+        const int i = k - LMIN;
+        if ((uint32_t)(k + 1) <= len) ja[i] = p0[k + 1];
+        a1 = ja[i];
+      }
+      acc[k] ^= __funnelshift_r(a0, a1, d);
+      a0 = a1;
+    }
+  }
+  uint32_t x[G::TP > 0 ? G::TP : 1];
+#pragma unroll
+  for (uint32_t i = 0; i < (G::TP > 0 ? G::TP : 1); i++) x[i] = 0;
+  if constexpr (G::TP > 0) {
+    // E[o + NB + i], i < TP, lane per index (ceil((j1 - j0) / 32) rounds, fixed by the level)
+    for (uint32_t jj = j0 + lane; jj < j1; jj += 32) {
+      const uint32_t d = dsm[jj];
+      const uint32_t *p = s1_window<P>(E + G::NB, d);
+      uint32_t w0 = p[0];
+      x[0] ^= __funnelshift_r(0u, w0, d);
+#pragma unroll
+      for (uint32_t i = 1; i < G::TP; i++) {
+        const uint32_t w1 = p[i];
+        x[i] ^= __funnelshift_r(w0, w1, d);
+        w0 = w1;
+      }
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < G::TP; i++) x[i] = __reduce_xor_sync(0xffffffffu, x[i]);
+  }
+  uint32_t nxt = __shfl_down_sync(0xffffffffu, pre, 1);
+  if constexpr (G::TP > 0) nxt = lane == 31 ? x[0] : nxt;
+  if (len == (uint32_t)L) acc[L - 1] ^= nxt;
+  top = 0;
+#pragma unroll
+  for (uint32_t i = 1; i < G::TP; i++) top = (uint32_t)lane == i - 1 ? x[i] : top;
+}
+
+// Stores of the segmented accumulators (the caller synchronises the warp first when rsm aliases E):
+// rsm[w] = acc (^ sv[w]) (^ xs[w]) for the lane's words w; starts distinct mod 32: conflict-free.
+template <class G, int MODE>
+__device__ __forceinline__ void s1_seg_store_impl(const uint32_t (&acc)[G::LMAX], uint32_t top, uint32_t *rsm,
+                                                  const uint32_t *xs, const uint32_t *sv, int lane) {
+  const uint32_t len = G::len(lane), st = G::start(lane);
+#pragma unroll
+  for (int k = 0; k < (int)G::LMAX; k++) {
+    if (k < (int)G::LMIN || (uint32_t)k < len) {
+      uint32_t x = acc[k];
+      if (MODE >= 1) x ^= sv[st + k];
+      if (MODE >= 2) x ^= xs[st + k];
+      rsm[st + k] = x;
+    }
+  }
+  if constexpr (G::TP > 1) {
+    if ((uint32_t)lane < G::TP - 1) {
+      uint32_t x = top;
+      if (MODE >= 1) x ^= sv[G::NB + lane];
+      if (MODE >= 2) x ^= xs[G::NB + lane];
+      rsm[G::NB + lane] = x;
+    }
+  }
+}
+template <class G>
+__device__ __forceinline__ void s1_seg_store(const uint32_t (&acc)[G::LMAX], uint32_t top, uint32_t *rsm, int lane) {
+  s1_seg_store_impl<G, 0>(acc, top, rsm, nullptr, nullptr, lane);
+}
+template <class G>
+__device__ __forceinline__ void s1_seg_store_xor(const uint32_t (&acc)[G::LMAX], uint32_t top, uint32_t *rsm,
+                                                 const uint32_t *sv, int lane) {
+  s1_seg_store_impl<G, 1>(acc, top, rsm, nullptr, sv, lane);
+}
+template <class G>
+__device__ __forceinline__ void s1_seg_store_xor2(const uint32_t (&acc)[G::LMAX], uint32_t top, uint32_t *rsm,
+                                                  const uint32_t *xs, const uint32_t *sv, int lane) {
+  s1_seg_store_impl<G, 2>(acc, top, rsm, xs, sv, lane);
 }
 
 }  // namespace hqc

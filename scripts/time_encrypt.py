@@ -13,6 +13,8 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2512_12904_b200 import gen, hqc  # noqa: E402
 
+hqc.LIB_PATH = os.environ.get("HQC_LIB", hqc.LIB_PATH)  # A/B of experiment builds
+
 
 def main(B=65536, levels=(1, 3, 5)):
     dev = torch.device("cuda:0")
