@@ -72,6 +72,10 @@ __device__ __forceinline__ void tma_store_1d(void *dst, const void *src, uint32_
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// Bulk prefetch of a global row into L2 (no shared memory, no completion): bytes a multiple of 16.
+__device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }

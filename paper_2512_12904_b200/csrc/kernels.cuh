@@ -925,6 +925,100 @@ __global__ void __launch_bounds__(512, 1) k_decrypt_s12(const uint64_t *__restri
 }
 
 
+// K4c (round 2, HQC-5 at large batches): K4x's first launch in a COMPACT per-warp layout. k_decrypt_s12 stages
+// v in a 7.2 KB buffer next to E (22.8 KB per warp: 9 warps per SM), and the warps that are in stage 2 leave
+// the shared-memory pipe to the others. Here v is not staged at all: its row is prefetched into L2 (a bulk
+// prefetch, no shared memory) when the product starts, r = u*y is stored above u's row in E (16-byte
+// aligned; the product is done reading E), the next u lands below it by TMA during stage 2, and stage 2
+// XORs v into each RM block straight from global memory (L2 hits) — 15.5 KB per warp, 14 warps per SM.
+template <class P> struct CxSmem {
+  using S = DecShape<P>;
+  using G = DecSeg<P>;
+  static constexpr uint32_t UB = P::U_STRIDE * 8, YB = P::Y_STRIDE * 4, VB = P::V_WORDS * 8;
+  static constexpr uint32_t R_OFF = round_up(UB, 16) / 4;  // r's first word, above u's row
+  static constexpr uint32_t EW0 = G::E_NEED > R_OFF + P::NW ? G::E_NEED : R_OFF + P::NW;
+  static constexpr uint32_t E_WORDS = round_up(EW0 > 2 * P::Q0 + 2 ? EW0 : 2 * P::Q0 + 2, 4);
+  static constexpr uint32_t E_BYTES = E_WORDS * 4;
+  static constexpr uint32_t Y_BYTES = round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t WARP_BYTES = E_BYTES + Y_BYTES + D_BYTES + 16;
+  static constexpr uint32_t bytes(uint32_t g) { return 16 + g * WARP_BYTES; }
+  static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
+  static constexpr uint32_t MAX_G = fit(16);
+  static_assert(VB % 16 == 0 && (P::N2 / 8) % 16 == 0, "v rows and RM blocks are whole 16-byte chunks");
+};
+
+template <class P>
+__global__ void __launch_bounds__(512, 1) k_decrypt_s12c(const uint64_t *__restrict__ u, const uint64_t *__restrict__ v,
+                                                         const uint32_t *__restrict__ y, uint8_t *__restrict__ sym_out,
+                                                         size_t batch) {
+  using M = CxSmem<P>;
+  using S = DecShape<P>;
+  using G = DecSeg<P>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t NG = blockDim.x >> 5;
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem);
+  uint8_t *ws = smem + 16 + (size_t)wib * M::WARP_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
+  uint32_t *Rr = E + M::R_OFF;
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::Y_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ws + M::E_BYTES + M::Y_BYTES + M::D_BYTES);
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  auto issue_uy = [&](size_t c) {
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, M::UB + M::YB);
+      tma_load_1d(E, u + c * P::U_STRIDE, M::UB, bar);
+      tma_load_1d(stg_y, y + c * P::Y_STRIDE, M::YB, bar);
+    }
+  };
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) issue_uy(ct);
+  if (threadIdx.x == 0) *next_item = NG;
+  __syncthreads();
+  uint32_t ph = 0;
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    const bool more = nct < c1;
+    mbar_wait(bar, ph);
+    ph ^= 1u;
+    if (lane == 0) tma_prefetch_l2(v + ct * P::V_WORDS, M::VB);  // v reaches L2 during the product
+    s1_stage_d<P, S>(stg_y, dsm, lane);
+    s1_build_E_upper<P, M>(E, lane);
+    __syncwarp();
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    __syncwarp();  // E, the support row and the rotation amounts are read
+    s1_seg_store<G>(acc, top, Rr, lane);  // r above u's row
+    if (more) issue_uy(nct);              // the next u lands below it during stage 2
+    __syncwarp();
+    uint8_t *dst = sym_out + ct * P::N1;
+    const uint4 *vg = reinterpret_cast<const uint4 *>(v + ct * P::V_WORDS);
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2: lane per RM block of r ^ v
+      const uint4 *src = reinterpret_cast<const uint4 *>(Rr) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        const uint4 w = __ldg(vg + j * (P::N2 / 128) + c);
+        X[4 * c] = x.x ^ w.x; X[4 * c + 1] = x.y ^ w.y; X[4 * c + 2] = x.z ^ w.z; X[4 * c + 3] = x.w ^ w.w;
+      }
+      dst[j] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+    __syncwarp();  // r is consumed: the next E build may overwrite it
+    ct = nct;
+  }
+}
+
+
 // K4p: small batches with a warp PAIR per decryption (configs[0]: 1,024 decryptions are 7 per SM, and a
 // launch is the latency of one decryption: product ~10k cycles — the SM's shared memory saturated by its 7
 // products — stage 2 6.6k in two rounds of 32 lanes, stage 3 ~10.7k; profiles/r02/sb_phases*.log). The pair
@@ -1505,13 +1599,13 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
 // 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p),
 // 8 = compact lane-RS warps (K4l), 9 = K4l with static per-warp ranges, 10 = stages 1+2 and stage 3 as two
-// launches (K4x). HQC_DEC_KERNEL=1..10 overrides.
+// launches (K4x), 11 = K4x with the compact first launch (K4c). HQC_DEC_KERNEL=1..11 overrides.
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 10 ? env : 0;
+  return env >= 1 && env <= 11 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1553,7 +1647,9 @@ template <class P> static int dec_kernel_for(int sms, size_t batch) {
   if (dec_kernel_env()) return dec_kernel_env();
   if (batch <= sp_max_batch<P>(sms)) return 7;
   if (batch <= sb_max_batch<P>(sms)) return 5;
-  return batch >= x_min_batch<P>(sms) ? 10 : dec_kernel<P>();
+  // K4c rather than K4x: 14 compact warps per SM instead of 9 (262,144: 9.10 vs 9.30 ms; 1,048,576: 36.04 vs
+  // 36.84; 131,072: 4.63 vs 4.75 — profiles/r02/ab_k4c.log)
+  return batch >= x_min_batch<P>(sms) ? 11 : dec_kernel<P>();
 }
 // The largest group (warps per CTA) of K4s whose shared memory fits one CTA.
 template <class P> constexpr uint32_t sb_max_g() {
@@ -1617,6 +1713,8 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_stage1<P>, 32 * stage1_g<P>(), stage1_smem<P>())) != cudaSuccess) return e;
   di.cap_stage1[P::level] = c > 0 ? c : 1;
   if ((e = cudaFuncSetAttribute(k_decrypt_s12<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_decrypt_s12c<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                CxSmem<P>::bytes(CxSmem<P>::MAX_G))) != cudaSuccess) return e;
   if (!di.pool) {  // the library's own pool (the device's default pool and its release threshold stay the caller's)
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
@@ -1680,6 +1778,15 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > stage1_g<P>()) g = stage1_g<P>();
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
+    return;
+  }
+  if (kind == 11) {  // k_decrypt_s12c: one CTA of up to CxSmem::MAX_G warps per SM; *per = warps per CTA
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > CxSmem<P>::MAX_G) g = CxSmem<P>::MAX_G;
     *per = g;
     const size_t groups = (batch + g - 1) / g;
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
@@ -1776,6 +1883,16 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
         return HQC_ERR_CUDA;
       k_decrypt_s12<P><<<grid, 32 * (unsigned)per, S1kSmem<P>::bytes((uint32_t)per), st>>>(
           u, v, y, sym, batch, (uint32_t)env_long("HQC_S12_STAGGER", 0));
+      const int rc = launch_stage3_on<P>(di, sym, m, nullptr, batch, st);
+      const bool freed = cudaFreeAsync(sym, st) == cudaSuccess;
+      if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
+      break;
+    }
+    case 11: {  // K4c: the compact stages 1+2 -> symbols in a pool scratch -> stage 3
+      uint8_t *sym = nullptr;
+      if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&sym), batch * P::N1, di->pool, st) != cudaSuccess)
+        return HQC_ERR_CUDA;
+      k_decrypt_s12c<P><<<grid, 32 * (unsigned)per, CxSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, sym, batch);
       const int rc = launch_stage3_on<P>(di, sym, m, nullptr, batch, st);
       const bool freed = cudaFreeAsync(sym, st) == cudaSuccess;
       if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
@@ -1934,7 +2051,7 @@ template <class P> static long long nlaunch_impl(size_t batch) {
   long long n = 0;
   for (size_t off = 0; off < batch; off += step) {
     const size_t c = batch - off < step ? batch - off : step;
-    n += dec_kernel_for<P>(di->sms, c) == 10 ? 2 : 1;
+    n += (dec_kernel_for<P>(di->sms, c) == 10 || dec_kernel_for<P>(di->sms, c) == 11) ? 2 : 1;
   }
   return n;
 }
@@ -1947,7 +2064,7 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
   *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
-        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10) ? (int)per : kind == 7 ? 2 * (int)per : 4;
+        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10 || kind == 11) ? (int)per : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

@@ -239,7 +239,9 @@ KERNEL_NAMES = {1: "k_decrypt_w1 (fused, one warp per ciphertext range, lane-per
                 7: "k_decrypt_sp (fused, warp pair per ciphertext, small batches)",
                 8: "k_decrypt_wl (fused, compact warps: v above u in E, chunks of 32, lane-per-word RS)",
                 9: "k_decrypt_wl<static> (fused, compact warps, per-warp contiguous ranges)",
-                10: "k_decrypt_s12 + k_stage3 (stages 1+2, symbols via HBM, lane-per-word RS: two launches)"}
+                10: "k_decrypt_s12 + k_stage3 (stages 1+2, symbols via HBM, lane-per-word RS: two launches)",
+                11: "k_decrypt_s12c + k_stage3 (compact stages 1+2: r above u in E, v from L2; symbols via HBM, "
+                    "lane-per-word RS: two launches)"}
 
 
 def hqc_decrypt_launch_kernel(level: int, batch: int) -> int:

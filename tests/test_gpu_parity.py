@@ -267,10 +267,10 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9", "10"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
     """Every decrypt kernel (hqc.KERNEL_NAMES; the library picks one per level and batch)
-    against the oracle on every level, including 10, the two-launch split with its pool scratch.
+    against the oracle on every level, including 10 and 11, the two-launch splits with their pool scratch.
     HQC_DEC_KERNEL forces each (read once per process), so each runs in a subprocess."""
     import subprocess
     import sys
@@ -300,8 +300,9 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_two_launch_kernel_ragged_split_and_graph_capture():
-    """Kernel 10 (k_decrypt_s12 + k_stage3, HQC-5's large-batch default) takes its symbol scratch from the
+@pytest.mark.parametrize("kernel", ["10", "11"])
+def test_two_launch_kernel_ragged_split_and_graph_capture(kernel):
+    """Kernels 10 and 11 (k_decrypt_s12 / _s12c + k_stage3, HQC-5's large-batch kernels) take their symbol scratch from the
     library's stream-ordered pool: split into ragged parts (HQC_DEC_SPLIT=1000 over 2,500 rows: 1000,
     1000, 500) it matches the oracle, and the call captured in a CUDA graph (pool allocation inside the
     capture) replays to the same outputs; a mixed-level call after it is unaffected."""
@@ -315,11 +316,12 @@ sys.path.insert(0, "tests")
 import oracle
 from paper_2512_12904_b200 import hqc
 from workloads import valid_batch
+KERNEL = int(sys.argv[1])
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
 for level in (5, 1):
     W = valid_batch(level, 90000, 2500, 41)
     p = hqc.params(level)
-    assert hqc.hqc_decrypt_launch_kernel(level, 2500) == 10
+    assert hqc.hqc_decrypt_launch_kernel(level, 2500) == KERNEL
     assert hqc.hqc_decrypt_launch_count(level, 2500) == 6
     u, v, y = d(W["u"]), d(W["v"]), d(W["y"])
     ref = oracle.decrypt_batch(W["params"], W["u"], W["v"], W["y"])
@@ -342,8 +344,8 @@ for level in (5, 1):
 print("ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, HQC_DEC_KERNEL="10", HQC_DEC_SPLIT="1000")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, HQC_DEC_KERNEL=kernel, HQC_DEC_SPLIT="1000")
+    r = subprocess.run([sys.executable, "-c", code, kernel], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
