@@ -209,7 +209,7 @@ __device__ __forceinline__ void warp_product_seg(uint32_t *su, const uint32_t *s
   s1_build_E<P, S>(su, E, lane);
   __syncwarp();
   uint32_t acc[G::LMAX], top;
-  s1_seg_product<P, G>(E, dsm, acc, top, lane);
+  s1_seg_product<P, G, s1_unroll_enc<P>()>(E, dsm, acc, top, lane);
   __syncwarp();
   s1_seg_store<G>(acc, top, E, lane);
   __syncwarp();
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
       using G = FullSeg<P>;
       static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
       uint32_t acc[G::LMAX], top;
-      s1_seg_product<P, G>(E, dsm, acc, top, lane);
+      s1_seg_product<P, G, s1_unroll_enc<P>()>(E, dsm, acc, top, lane);
       out_free();
       s1_seg_store<G>(acc, top, out, lane);
 #else
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(64 * Enc2Smem<P>::MAX_Q, HQC_ENC2_MINB) k_encr
       using G = EncVSeg<P>;
       static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
       uint32_t acc[G::LMAX], top;
-      s1_seg_product<P, G>(E, dsm, acc, top, lane);
+      s1_seg_product<P, G, s1_unroll_enc<P>()>(E, dsm, acc, top, lane);
       out_free();
       s1_seg_store<G>(acc, top, out, lane);
 #else

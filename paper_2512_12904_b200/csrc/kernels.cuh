@@ -140,7 +140,7 @@ template <class P> struct S1Pipe {
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
     uint32_t acc[G::LMAX], top;
-    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane);
     __syncwarp();  // every lane is done reading E: r overwrites it
     PHASE(3);
     if (v) {
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(512, HQC_S1K_MINB) k_stage1(const uint64_t *__
     const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
     if (lane == 0) tma_store_wait_read();  // the previous r (in the staging buffer) has been read by its store
     __syncwarp();
-    pipe.run(ct, nct < c1, nct, lane);
+    pipe.template run<s1_unroll_s1<P>()>(ct, nct < c1, nct, lane);
     fence_proxy_async_smem();  // r -> HBM by a TMA bulk store, asynchronous to the next product
     __syncwarp();
     if (lane == 0) tma_store_1d(r_out + ct * P::V_WORDS, pipe.stg, P::V_WORDS * 8);
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
     uint32_t acc[G::LMAX], top;
-    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane);
 #else
     uint32_t acc[ST::R];
     s1_product<P, ST>(E, dsm, acc, lane);
@@ -748,6 +748,8 @@ template <class P> struct SbPipe {
   // E from the u row already in its lower half (stage1.cuh: s1_build_E_upper)
   __device__ __forceinline__ void build_E(int lane) { s1_build_E_upper<P, DecShape<P>>(E, lane); }
   // Stage 1 of ct (its u, y requested); leaves r in stg; requests next's u, y as soon as E is read.
+  // U: the product's index-pair unroll (0: the fused kernels' s1_unroll_dec; k_stage1 passes its own).
+  template <int U = 0>
   __device__ __forceinline__ void run(size_t ct, bool has_next, size_t next, int lane) {
     using S = DecShape<P>;
     using ST = DecShapeT<P>;
@@ -769,7 +771,7 @@ template <class P> struct SbPipe {
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
     uint32_t acc[G::LMAX], top;
-    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    s1_seg_product<P, G, (U ? U : s1_unroll_dec<P>())>(E, dsm, acc, top, lane);
     __syncwarp();  // every lane is done reading E (and dsm, stg_y): the next rows may land
     PHASE(3);
     if (has_next) issue_uy(next, lane);
@@ -995,7 +997,7 @@ __global__ void __launch_bounds__(512, 1) k_decrypt_s12c(const uint64_t *__restr
     s1_build_E_upper<P, M>(E, lane);
     __syncwarp();
     uint32_t acc[G::LMAX], top;
-    s1_seg_product<P, G>(E, dsm, acc, top, lane);
+    s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane);
     __syncwarp();  // E, the support row and the rotation amounts are read
     s1_seg_store<G>(acc, top, Rr, lane);  // r above u's row
     if (more) issue_uy(nct);              // the next u lands below it during stage 2
@@ -1103,7 +1105,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
     uint32_t acc[G::LMAX], top;
-    s1_seg_product<P, G>(E, dsm, acc, top, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
+    s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
     if (wa) s1_seg_store<G>(acc, top, X, lane);
     pair_sync(bid);  // both warps are done with E; B's image is in X
     if (wa == 0) {

@@ -37,6 +37,36 @@ template <class P> constexpr int s1_unroll() {
 #endif
 }
 
+// Index-pair unroll of the segmented product (s1_seg_product), per kernel family, measured against the
+// R-word values above after the layout change (profiles/r02/ab_unroll*.log): the fused decrypt kernels
+// want 2 at every level (HQC-5 K4c 8.61 vs 9.21 ms with 3: the 3-pair body of 57-word windows thrashed
+// the instruction cache, 12.5% no_instruction stalls), the standalone product 3 (HQC-1 / 3 / 5 -0.8 /
+// -1.0 / -1.1%).
+template <class P> constexpr int s1_unroll_dec() {
+#ifdef HQC_S1_UNROLL_DEC
+  return HQC_S1_UNROLL_DEC;
+#else
+  return 2;
+#endif
+}
+template <class P> constexpr int s1_unroll_s1() {
+#ifdef HQC_S1_UNROLL_S1
+  return HQC_S1_UNROLL_S1;
+#else
+  return 3;
+#endif
+}
+
+// Encrypt / KeyGen products: HQC-3 prefers 3 (1.99 vs 2.06 ms per 65,536 encryptions), HQC-5 2 (4.33 vs
+// 4.36), HQC-1 either (profiles/r02/ab_unroll_enc.log).
+template <class P> constexpr int s1_unroll_enc() {
+#ifdef HQC_S1_UNROLL_ENC2
+  return HQC_S1_UNROLL_ENC2;
+#else
+  return P::level == 3 ? 3 : 2;
+#endif
+}
+
 // Build E (S::E_WORDS words) from the staged dense row su (shared memory):
 //   E[q] = u32[q]                                   q < Q0
 //   E[Q0] = (last C bits of u) | u32[0] << C        the wrap of X^n = 1
@@ -472,7 +502,7 @@ template <class P> using EncVSeg = SegShape<P, P::NW, P::WR>;      // s*r2 trunc
 
 // The product over support indices [j0, j1) (j0 even) in the segmented layout: acc[k] = output word
 // st_L + k for k < len_L (complete, the neighbour's part included); `top` = word NB + lane for lane < TP - 1.
-template <class P, class G>
+template <class P, class G, int UNROLL = s1_unroll<P>()>
 __device__ __forceinline__ void s1_seg_product(const uint32_t *E, const uint32_t *dsm, uint32_t (&acc)[G::LMAX],
                                                uint32_t &top, int lane, uint32_t j0 = 0, uint32_t j1 = G::WT) {
   constexpr int L = (int)G::LMAX, LMIN = (int)G::LMIN;
@@ -488,7 +518,7 @@ __device__ __forceinline__ void s1_seg_product(const uint32_t *E, const uint32_t
 #pragma unroll
   for (int i = 0; i < NPS; i++) ja[i] = jb[i] = 0;
   uint32_t j = j0;
-  constexpr int kUnroll = s1_unroll<P>();
+  constexpr int kUnroll = UNROLL;
 #pragma unroll kUnroll
   for (; j + 1 < j1; j += 2) {
     const uint2 dd = *reinterpret_cast<const uint2 *>(dsm + j);
