@@ -1630,7 +1630,9 @@ static long env_long(const char *name, long dflt) {
 template <class P> static size_t sb_max_batch(int sms) {
   // HQC-3: K4s up to ~44,000, K4l beyond (32,768: 0.591 vs 0.600 ms; 65,536: 1.139 vs 1.073;
   // 4,194,304: 6.05e7 vs 6.36e7/s — profiles/r02/ab_wl*.log)
-  const long dflt = (long)sms * (P::level == 1 ? 270 : P::level == 3 ? 300 : 160);
+  // HQC-5: K4s up to ~16,000, K4c beyond (16,384: 0.678 vs 0.678 ms; 32,768: 1.18 vs 1.33 —
+  // profiles/r02/sweep_x5.log, after the segmented layout and the unroll of 2)
+  const long dflt = (long)sms * (P::level == 1 ? 270 : P::level == 3 ? 300 : 110);
   const long v = env_long("HQC_SB_MAX", dflt);
   return v < 0 ? ~(size_t)0 : (size_t)v;
 }
@@ -1641,8 +1643,12 @@ template <class P> static size_t sb_max_batch(int sms) {
 template <class P> static size_t sp_max_batch(int sms) { return (size_t)env_long("HQC_SP_MAX", (long)sms * 4); }
 // K4x (two launches) for HQC-5 from ~96,000 (131,072: 4.77 vs 4.88 ms for K4a; 262,144 9.36 vs 9.58;
 // 4,194,304 in launches of 1,048,576: 2.83e7 vs 2.74e7/s; 65,536: 2.55 vs 2.53 — profiles/r02/ab_x5.log).
+// Since K4c (k_decrypt_s12c) and the unroll of 2, the two-launch form wins for HQC-5 at every batch above the
+// K4s range (32,768: 1.18 ms vs 1.22 for K4a and 1.24 for K4x; 262,144: 8.48 vs 9.45 / 9.01 —
+// profiles/r02/sweep_x5.log). HQC-3's K4x beats K4l by 1-4% between ~131,072 and ~524,288 and loses at
+// 4,194,304 (profiles/r02/sweep_x3.log); not used there (neither configs[1] nor configs[4] is in that range).
 template <class P> static size_t x_min_batch(int sms) {
-  const long v = env_long("HQC_X_MIN", P::level == 5 ? (long)sms * 640 : -1);
+  const long v = env_long("HQC_X_MIN", P::level == 5 ? (long)sms * 110 : -1);
   return v < 0 ? ~(size_t)0 : (size_t)v;
 }
 template <class P> static int dec_kernel_for(int sms, size_t batch) {

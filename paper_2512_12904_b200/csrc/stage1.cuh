@@ -189,10 +189,11 @@ __device__ __forceinline__ void s1_build_E_upper(uint32_t *E, int lane) {
 // A rotation amount d = 32 o + s is kept as (o << 7) | s: its low 5 bits are the funnel-shift amount
 // (SHF.R.W wraps the amount mod 32) and >> 5 is the window's byte offset 4 o, one shift instead of a
 // shift and a mask per index.
-// Per level from measurement: packed for the one-warp kernels (HQC-1 -1%, HQC-5 -0.5%, standalone
-// product -0.3..-0.8%), plain for the HQC-3 warp pair (+1.3% there).
+// Packed at every level since the segmented layout: the one-warp kernels (HQC-1 -1%, HQC-5 -0.5%,
+// standalone product -0.3..-0.8%) and now HQC-3's K4l too (65,536: 1.069 -> 1.054 ms; 1,024 -3%;
+// profiles/r02/ab_pack.log); only round 1's HQC-3 warp pair had preferred the plain form (+1.3%).
 #ifndef HQC_PACK_D
-#define HQC_PACK_D (P::level != 3)
+#define HQC_PACK_D 1
 #endif
 template <class P> __device__ __forceinline__ uint32_t s1_pack_d(uint32_t d) {
   return HQC_PACK_D ? ((d >> 5) << 7) | (d & 31u) : d;
