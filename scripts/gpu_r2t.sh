@@ -1,5 +1,7 @@
-# the N = 2 bench path (torchrun, two ranks) on ONE GPU with gloo collectives: a logic check, not a measurement
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-HQC_BENCH_BACKEND=gloo timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 --no-variants --config5-total 1048576 > gpurun_out/bench_n2_gloo.log 2>&1
-echo "exit $?" >> gpurun_out/bench_n2_gloo.log
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_t.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu_t.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_t.log 2>&1; echo "exit $?" >> gpurun_out/smoke_t.log
+timeout 900 python bench.py > gpurun_out/bench_t.log 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_t.log 2>&1
+timeout 600 python scripts/time_stages.py > gpurun_out/time_stages_t.log 2>&1
