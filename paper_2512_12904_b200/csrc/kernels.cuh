@@ -547,6 +547,13 @@ __global__ void __launch_bounds__(32 * WdSmem<P>::MAX_G, 1) k_decrypt_wd(const u
 // next u lands below it. Per warp: E, the support row, the rotation amounts, the symbol chunk — HQC-3
 // 11.8 KB (16 warps per SM), HQC-5 19.3 KB (11). The CTA's warps share its range through a counter (K4d).
 // The v fetch is not hidden behind this warp's product (it cannot land earlier); other warps hide it.
+// K4l's v: 1 = not staged — prefetched into L2 when the product starts and XORed into each RM block by
+// stage 2 straight from global memory (as in K4c); 0 = fetched by TMA after the product into the region
+// above u's row, where r is then formed in place. Measured (profiles/r02/ab_vl2.log): 65,536 +0.2%,
+// 262,144 +0.8%, 4,194,304 -1.2% with 1 — no clear gain, so 0 (an experiment switch).
+#ifndef HQC_WL_VL2
+#define HQC_WL_VL2 0
+#endif
 template <class P> struct WlSmem {
   using S = DecShape<P>;
   static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
@@ -631,6 +638,9 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     s1_stage_d<P, S>(stg_y, dsm, lane);
     s1_build_E_upper<P, S>(E, lane);  // the shifted upper copy of E from u's row in its lower half
     __syncwarp();
+#if HQC_WL_VL2
+    if (lane == 0) tma_prefetch_l2(v + ct * P::V_WORDS, M::VB);  // v reaches L2 during the product
+#endif
 #if HQC_S1_SEG
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
@@ -648,6 +658,12 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     }
 #endif
     __syncwarp();  // E is read: v may land above u's row, the next u in it
+#if HQC_WL_VL2 && HQC_S1_SEG
+    if (more) issue_uy(nct);
+    if (lane == 0) cidx[slot] = (uint32_t)(ct - cbase);
+    s1_seg_store<G>(acc, top, Rv, lane);  // u*y above u's row; stage 2 adds v from L2
+    (void)ph_v;
+#else
     if (lane == 0) {
       fence_proxy_async_smem();
       mbar_expect_tx(bar + 1, M::VB);
@@ -657,19 +673,28 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
     if (lane == 0) cidx[slot] = (uint32_t)(ct - cbase);
     mbar_wait(bar + 1, ph_v);
     ph_v ^= 1u;
-#if HQC_S1_SEG
+#endif
+#if HQC_S1_SEG && HQC_WL_VL2
+#elif HQC_S1_SEG
     s1_seg_store_xor<G>(acc, top, Rv, Rv, lane);  // r = acc ^ v in place
 #else
     s1_store_r_xor<ST>(acc, Rv, Rv, lane);  // r = acc ^ v in place
     if (TW > 0 && (uint32_t)lane < TW) Rv[ST::NOUT + lane] = mine ^ Rv[ST::NOUT + lane];
 #endif
     __syncwarp();
+#if HQC_WL_VL2 && HQC_S1_SEG
+    const uint4 *vg = reinterpret_cast<const uint4 *>(v + ct * P::V_WORDS);
+#endif
     for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2 into the chunk's slot
       const uint4 *src = reinterpret_cast<const uint4 *>(Rv) + j * (P::N2 / 128);
       uint32_t X[P::MULT * 4];
 #pragma unroll
       for (int c = 0; c < (int)P::MULT; c++) {
-        const uint4 x = src[c];
+        uint4 x = src[c];
+#if HQC_WL_VL2 && HQC_S1_SEG
+        const uint4 w = __ldg(vg + j * (P::N2 / 128) + c);
+        x.x ^= w.x; x.y ^= w.y; x.z ^= w.z; x.w ^= w.w;
+#endif
         X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
       }
       sb[j * M::SYM_PITCH + slot] = (uint8_t)rm_decode_block<P::MULT>(X);
