@@ -342,7 +342,12 @@ __global__ void __launch_bounds__(128) k_stage2(const uint64_t *__restrict__ r, 
 // K3: stage 3 alone. One thread per ciphertext; a warp stages its 32 rows of symbols into shared
 // memory as [j][lane] so every later access is conflict-free.
 template <class P>
-__global__ void __launch_bounds__(128) k_stage3(const uint8_t *__restrict__ sym, uint8_t *__restrict__ m_out,
+// k_stage3's register cap: 4 CTAs of 128 threads per SM (<= 128 registers, no spills; uncapped it took 158
+// and 3 CTAs): HQC-5 stage 3 alone 0.84 -> 0.77 ms per 262,144 (profiles/r02/ab_s3.log); 5 CTAs spill.
+#ifndef HQC_S3_MINB
+#define HQC_S3_MINB 4
+#endif
+__global__ void __launch_bounds__(128, HQC_S3_MINB) k_stage3(const uint8_t *__restrict__ sym, uint8_t *__restrict__ m_out,
                                                 uint8_t *__restrict__ ok_out, size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);

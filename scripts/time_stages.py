@@ -13,6 +13,8 @@ import torch  # noqa: E402
 from bench import make_valid_workload  # noqa: E402
 from paper_2512_12904_b200 import hqc  # noqa: E402
 
+hqc.LIB_PATH = os.environ.get("HQC_LIB", hqc.LIB_PATH)  # A/B of experiment builds
+
 
 def timed(fn, steps=20, warm=3):
     for _ in range(warm):
