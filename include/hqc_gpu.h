@@ -90,13 +90,14 @@ const char *hqc_status_str(int status);
  * The launch policy picks the kernel by level and batch (hqc_decrypt_launch_kernel
  * reports it): one fused kernel — stage 1 in shared memory, stage 2 lane-per-RM-block, stage 3 by a
  * warp per word (small batches) or a lane per word (large ones), no intermediate leaving the SM — except
- * HQC-5 at large batches (kernel 10), which runs stages 1+2 in one launch, writes the n1 received
- * symbols of each ciphertext to a scratch buffer and decodes them in a second launch. That scratch
+ * HQC-5 above ~16,000 (kernel 11; kernel 10 is its round-2 predecessor), which runs stages 1+2 in
+ * one launch, writes the n1 received symbols of each ciphertext to a scratch buffer and decodes them
+ * in a second launch. That scratch
  * (batch x n1 bytes, at most 1,048,576 rows per launch) comes from a memory pool the library creates
  * per device on first use; it is stream-ordered (allocated and freed on `stream`, so concurrent calls
  * on different streams are safe and the call can be captured in a CUDA graph) and the pool keeps freed
  * memory for later calls (up to ~94 MB). A large batch may run as consecutive launches
- * (hqc_decrypt_launch_count). All default kernels are constant-flow (R#8). HQC_DEC_KERNEL=1..10
+ * (hqc_decrypt_launch_count). All default kernels are constant-flow (R#8). HQC_DEC_KERNEL=1..11
  * forces a kernel (same results; 4 is the tensor-memory product, whose loop counts depend on y,
  * DESIGN.md §6.1b); the variable is read once per process.
  * ------------------------------------------------------------------------------------------- */

@@ -1,4 +1,21 @@
+# round 2 (session 3): final-state tests, bench, reference arm, ncu
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_encrypt.py tests/test_gpu_kem.py -m gpu -q -x > gpurun_out/pytest_enc3.log 2>&1; echo "exit $?" >> gpurun_out/pytest_enc3.log
-timeout 600 python scripts/time_encrypt.py > gpurun_out/time_enc3.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_u.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu_u.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_u.log 2>&1; echo "exit $?" >> gpurun_out/smoke_u.log
+timeout 900 python bench.py > gpurun_out/bench_u.log 2>&1
+timeout 900 torchrun --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 10 --warmup 3 > gpurun_out/bench_torchrun_u.log 2>&1
+run() {  # name, kernel regex, command...
+  local name=$1 rx=$2; shift 2
+  timeout 300 "$@" > gpurun_out/u_plain_$name.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$rx -s 3 -c 1 -o gpurun_out/u_$name "$@" > gpurun_out/u_ncu_$name.log 2>&1
+  echo "$name exit $?" >> gpurun_out/u_status.log
+}
+run fused_L5 k_decrypt_s12c python scripts/prof_kernels.py --level 5 --batch 262144 --only fused --iters 2
+run stage3_L5 k_stage3 python scripts/prof_kernels.py --level 5 --batch 262144 --only fused --iters 2
+run fused_L3 k_decrypt python scripts/prof_kernels.py --level 3 --batch 65536 --only fused --iters 2
+run enc_L1 k_encrypt2 python scripts/time_encrypt.py
+CMD="python bench.py --steps 5 --warmup 3 --no-configs --no-levels --no-variants --no-cpu-baseline"
+timeout 600 $CMD > gpurun_out/u_bench_plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/u_launches.csv $CMD > gpurun_out/u_ncu_launches.log 2>&1
+echo "launches exit $?" >> gpurun_out/u_status.log
