@@ -722,6 +722,191 @@ __global__ void __launch_bounds__(32 * WlSmem<P>::MAX_G, 1) k_decrypt_wl(const u
 }
 
 
+// K4w (round 2, session 3; opt-in, HQC_DEC_KERNEL=12): K4l with the RS chunks SHARED by the CTA. Measured
+// against K4l (profiles/r02/ab_wc.log, ab_wc2.log): HQC-3 65,536 1.081 vs 1.046 ms (slower), 262,144 4.08
+// vs 4.24 (faster), 4,194,304 equal; HQC-1 12% slower than K4d. Neither BASELINE size gains, so not a default. K4l decodes a warp's own chunk of 32
+// when it is full or the warp's work runs out; at 65,536 HQC-3 ciphertexts a warp gets ~28, so every chunk
+// is decoded at the very end of the launch, all 16 warps of an SM at once with no product left to overlap
+// (~40 us of a 1.05 ms launch; 4,194,304 runs at 0.86 of the roofline against 0.83). Here a chunk is 32
+// CONSECUTIVE ciphertexts of the CTA's range, whichever warps decrypt them: stage 2 writes each symbol row
+// into a ring of R chunk buffers shared by the CTA, a per-buffer counter counts the rows in, and the warp
+// that completes a chunk decodes it at once (lane per word, its outputs contiguous), while the other warps
+// keep multiplying. Only the CTA's last chunk is decoded at the end. A warp about to write into a buffer
+// first waits (rarely) until the chunk R places earlier has been decoded out of it; the oldest chunk
+// always completes, so no warp waits forever. The instruction stream is the same for every ciphertext.
+#ifndef HQC_WC_RING
+#define HQC_WC_RING 4
+#endif
+// The CTA's last chunk decoded word by word by the warp decoder of every idle warp (1) or by one lane decode
+// (0). Measured (profiles/r02/ab_wc2.log): no change at 65,536, slower at 262,144 (4.13 vs 4.08 ms): 0.
+#ifndef HQC_WC_WARPTAIL
+#define HQC_WC_WARPTAIL 0
+#endif
+template <class P> struct WcSmem {
+  using S = DecShape<P>;
+  static constexpr uint32_t UB = P::U_STRIDE * 8, VB = P::V_WORDS * 8, YB = P::Y_STRIDE * 4;
+  static constexpr uint32_t RB = VB > S3Scratch<P>::BYTES ? VB : S3Scratch<P>::BYTES;  // v, r, RS scratch
+  static constexpr uint32_t E_BYTES = round_up(S::E_WORDS * 4 > UB + RB ? S::E_WORDS * 4 : UB + RB, 16);
+  static constexpr uint32_t Y_BYTES = round_up(YB, 16);
+  static constexpr uint32_t D_BYTES = round_up(S::WPAD * 4, 16);
+  static constexpr uint32_t WARP_BYTES = E_BYTES + Y_BYTES + D_BYTES + 16;
+  static constexpr uint32_t RING = HQC_WC_RING;
+  static constexpr uint32_t SYM_PITCH = 36;  // odd word pitch: the 32 lanes' stage-2 byte stores hit 32 banks
+  static constexpr uint32_t BUF_BYTES = round_up(P::N1 * SYM_PITCH, 16);
+  static constexpr uint32_t CTL_BYTES = round_up(2 * RING * 4, 16);  // done[RING], gen[RING]
+  static constexpr uint32_t HEAD = GF_BYTES + 16 + CTL_BYTES + RING * BUF_BYTES;
+  static constexpr uint32_t bytes(uint32_t g) { return HEAD + g * WARP_BYTES; }
+  static constexpr uint32_t fit(uint32_t g) { return g > 1 && bytes(g) > 227u * 1024u ? fit(g - 1) : g; }
+  static constexpr uint32_t MAX_G = fit(16);
+  static_assert(UB % 16 == 0, "the v / r region starts 16-byte aligned above u's row");
+  static_assert(RING >= 2, "a ring of at least two chunk buffers");
+  static_assert(RB >= round_up(P::N1, 16) + RsWarpScratch<P>::BYTES, "the warp decoder's word and scratch fit above u");
+};
+
+template <class P>
+__global__ void __launch_bounds__(32 * WcSmem<P>::MAX_G, 1) k_decrypt_wc(const uint64_t *__restrict__ u,
+                                                                        const uint64_t *__restrict__ v,
+                                                                        const uint32_t *__restrict__ y,
+                                                                        uint8_t *__restrict__ m_out,
+                                                                        size_t batch) {
+  using M = WcSmem<P>;
+  using S = DecShape<P>;
+  using G = DecSeg<P>;
+  static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
+  extern __shared__ __align__(16) uint8_t smem[];
+  GfTables *gf = reinterpret_cast<GfTables *>(smem);
+  unsigned int *next_item = reinterpret_cast<unsigned int *>(smem + GF_BYTES);
+  unsigned int *done = reinterpret_cast<unsigned int *>(smem + GF_BYTES + 16);  // rows in, per buffer
+  volatile unsigned int *gen = done + M::RING;  // chunks decoded out of each buffer
+  uint8_t *ring = smem + GF_BYTES + 16 + M::CTL_BYTES;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t NG = blockDim.x >> 5;
+  uint8_t *ws = smem + M::HEAD + (size_t)wib * M::WARP_BYTES;
+  uint32_t *E = reinterpret_cast<uint32_t *>(ws);
+  uint32_t *Rv = reinterpret_cast<uint32_t *>(ws + M::UB);  // v, then r, then the RS scratch
+  uint32_t *stg_y = reinterpret_cast<uint32_t *>(ws + M::E_BYTES);
+  uint32_t *dsm = reinterpret_cast<uint32_t *>(ws + M::E_BYTES + M::Y_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ws + M::E_BYTES + M::Y_BYTES + M::D_BYTES);  // [0] u, y  [1] v
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncwarp();
+  auto issue_uy = [&](size_t c) {
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar, M::UB + M::YB);
+      tma_load_1d(E, u + c * P::U_STRIDE, M::UB, bar);
+      tma_load_1d(stg_y, y + c * P::Y_STRIDE, M::YB, bar);
+    }
+  };
+  const size_t per_cta = (batch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = (size_t)blockIdx.x * per_cta;
+  const size_t c1 = c0 + per_cta < batch ? c0 + per_cta : batch;
+  size_t ct = c0 + wib;
+  if (ct < c1) issue_uy(ct);
+  if (threadIdx.x == 0) next_item[0] = NG, next_item[1] = 0;  // work counter, last-chunk word counter
+  if (threadIdx.x < 2 * M::RING) done[threadIdx.x] = 0;  // done[] and gen[]
+  gf_tables_to_smem(gf);
+  __syncthreads();
+  const size_t nrows = c1 > c0 ? c1 - c0 : 0;
+  const uint32_t last_chunk = nrows ? (uint32_t)((nrows - 1) >> 5) : 0u;
+  uint32_t ph_uy = 0, ph_v = 0;
+  while (ct < c1) {
+    uint32_t nx = 0;
+    if (lane == 0) nx = atomicAdd(next_item, 1u);
+    const size_t nct = c0 + __shfl_sync(0xffffffffu, nx, 0);
+    const bool more = nct < c1;
+    mbar_wait(bar, ph_uy);
+    ph_uy ^= 1u;
+    s1_stage_d<P, S>(stg_y, dsm, lane);
+    s1_build_E_upper<P, S>(E, lane);
+    __syncwarp();
+    uint32_t acc[G::LMAX], top;
+    s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane);
+    __syncwarp();  // E is read: v may land above u's row, the next u in it
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(bar + 1, M::VB);
+      tma_load_1d(Rv, v + ct * P::V_WORDS, M::VB, bar + 1);
+    }
+    if (more) issue_uy(nct);
+    mbar_wait(bar + 1, ph_v);
+    ph_v ^= 1u;
+    s1_seg_store_xor<G>(acc, top, Rv, Rv, lane);  // r = acc ^ v in place
+    // this ciphertext's chunk, its slot and its buffer (row k of the CTA's range)
+    const size_t k = ct - c0;
+    const uint32_t chunk = (uint32_t)(k >> 5), slot = (uint32_t)(k & 31), b = chunk % M::RING;
+    uint8_t *sb = ring + (size_t)b * M::BUF_BYTES;
+    if (lane == 0)  // the chunk RING places earlier must have been decoded out of this buffer
+      while (gen[b] != chunk / M::RING) __nanosleep(64);
+    __syncwarp();
+    for (uint32_t j = lane; j < P::N1; j += 32) {  // stage 2 into the chunk's slot
+      const uint4 *src = reinterpret_cast<const uint4 *>(Rv) + j * (P::N2 / 128);
+      uint32_t X[P::MULT * 4];
+#pragma unroll
+      for (int c = 0; c < (int)P::MULT; c++) {
+        const uint4 x = src[c];
+        X[4 * c] = x.x; X[4 * c + 1] = x.y; X[4 * c + 2] = x.z; X[4 * c + 3] = x.w;
+      }
+      sb[j * M::SYM_PITCH + slot] = (uint8_t)rm_decode_block<P::MULT>(X);
+    }
+    __syncwarp();
+    const size_t cstart = c0 + ((size_t)chunk << 5);
+    const uint32_t csize = c1 - cstart < 32 ? (uint32_t)(c1 - cstart) : 32u;
+    uint32_t last = 0;
+    if (lane == 0) {
+      __threadfence_block();  // the row is visible before it is counted
+      last = atomicAdd(done + b, 1u) + 1u == csize;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0) && (!HQC_WC_WARPTAIL || chunk != last_chunk)) {  // decode it now
+      __threadfence_block();
+      for (uint32_t q = csize; q < 32; q++)
+        for (uint32_t j = lane; j < P::N1; j += 32) sb[j * M::SYM_PITCH + q] = 0;
+      __syncwarp();
+      auto sym_at = [&](int j) -> uint32_t { return sb[j * M::SYM_PITCH + lane]; };
+      rs_decode_lane<P>(sym_at, gf, reinterpret_cast<uint16_t *>(Rv), lane,
+                        (uint32_t)lane < csize ? m_out + (cstart + lane) * P::K : nullptr);
+      __syncwarp();
+      if (lane == 0) {
+        done[b] = 0;
+        __threadfence_block();
+        gen[b] = chunk / M::RING + 1;  // the buffer is free for chunk + RING
+      }
+    }
+    __syncwarp();
+    ct = nct;
+  }
+#if HQC_WC_WARPTAIL
+  // The CTA's last chunk: once its rows are all in, every warp that has run out of work takes words of it
+  // one at a time and decodes each with the whole warp (stage3_warp.cuh) — ~11k cycles per word instead of
+  // one lane decode of the whole chunk by a single warp (~20k dependent warp instructions).
+  if (nrows) {
+    const uint32_t b = last_chunk % M::RING;
+    const uint32_t csize = (uint32_t)(nrows - ((size_t)last_chunk << 5));
+    const uint8_t *sb = ring + (size_t)b * M::BUF_BYTES;
+    volatile unsigned int *vdone = done;
+    if (lane == 0)
+      while (vdone[b] < csize) __nanosleep(128);
+    __syncwarp();
+    __threadfence_block();
+    uint8_t *mysym = reinterpret_cast<uint8_t *>(Rv);
+    uint16_t *scr = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(Rv) + round_up(P::N1, 16));
+    while (true) {
+      uint32_t w = 0;
+      if (lane == 0) w = atomicAdd(next_item + 1, 1u);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= csize) break;
+      for (uint32_t j = lane; j < P::N1; j += 32) mysym[j] = sb[j * M::SYM_PITCH + w];
+      __syncwarp();
+      rs_decode_warp<P>(mysym, gf, scr, lane, m_out + (c0 + ((size_t)last_chunk << 5) + w) * P::K);
+      __syncwarp();
+    }
+  }
+#endif
+}
+
+
 // K4s: fused decrypt for SMALL batches (BASELINE configs[0]: HQC-1 at 1,024). K4a gives every warp at
 // least 16 consecutive ciphertexts, so a batch of 1,024 occupies 64 warps on 64 SMs and the launch is the
 // latency of 16 products in a row plus a lane-per-word RS decode. Here every warp takes ONE ciphertext at a
@@ -1631,13 +1816,14 @@ template <class P> static uint32_t decrypt_t_smem() { return TmDec<P>::M::SMEM_B
 // 2 = warp pair, 3 = warp-specialised, 4 = tensor-memory product (K4t), 5 = small-batch groups (K4s),
 // 6 = K4a with CTA-shared work (K4d), 7 = small batches with a warp pair per decryption (K4p),
 // 8 = compact lane-RS warps (K4l), 9 = K4l with static per-warp ranges, 10 = stages 1+2 and stage 3 as two
-// launches (K4x), 11 = K4x with the compact first launch (K4c). HQC_DEC_KERNEL=1..11 overrides.
+// launches (K4x), 11 = K4x with the compact first launch (K4c), 12 = K4l with CTA-shared RS chunks (K4w).
+// HQC_DEC_KERNEL=1..12 overrides.
 static int dec_kernel_env() {
   static int env = [] {
     const char *s = getenv("HQC_DEC_KERNEL");
     return s ? atoi(s) : 0;
   }();
-  return env >= 1 && env <= 11 ? env : 0;
+  return env >= 1 && env <= 12 ? env : 0;
 }
 template <class P> static int dec_kernel() {
   if (dec_kernel_env()) return dec_kernel_env();
@@ -1744,6 +1930,8 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
                                 WlSmem<P>::bytes(WlSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_wl<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WlSmem<P>::bytes(WlSmem<P>::MAX_G))) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_decrypt_wc<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WcSmem<P>::bytes(WcSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_wd<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 WdSmem<P>::bytes(WdSmem<P>::MAX_G))) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt_sb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1816,6 +2004,15 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > stage1_g<P>()) g = stage1_g<P>();
+    *per = g;
+    const size_t groups = (batch + g - 1) / g;
+    *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
+    return;
+  }
+  if (kind == 12) {  // k_decrypt_wc: one CTA of up to WcSmem::MAX_G warps per SM; *per = warps per CTA
+    size_t g = (batch + di.sms - 1) / (size_t)di.sms;
+    if (g < 1) g = 1;
+    if (g > WcSmem<P>::MAX_G) g = WcSmem<P>::MAX_G;
     *per = g;
     const size_t groups = (batch + g - 1) / g;
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
@@ -1926,6 +2123,9 @@ static int launch_decrypt_one(DevInfo *di, const uint64_t *u, const uint64_t *v,
       if (rc != HQC_OK || !freed) return HQC_ERR_CUDA;
       break;
     }
+    case 12:
+      k_decrypt_wc<P><<<grid, 32 * (unsigned)per, WcSmem<P>::bytes((uint32_t)per), st>>>(u, v, y, m, batch);
+      break;
     case 11: {  // K4c: the compact stages 1+2 -> symbols in a pool scratch -> stage 3
       uint8_t *sym = nullptr;
       if (cudaMallocFromPoolAsync(reinterpret_cast<void **>(&sym), batch * P::N1, di->pool, st) != cudaSuccess)
@@ -2102,7 +2302,8 @@ template <class P> static int shape_impl(size_t batch, int *grid, int *wpc) {
   decrypt_shape<P>(*di, batch, grid, &per);
   const int kind = dec_kernel_for<P>(di->sms, batch);
   *wpc = kind == 1 ? 1 : kind == 2 ? DEC_THREADS / 32 : kind == 4 ? TmDec<P>::WARPS
-        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10 || kind == 11) ? (int)per : kind == 7 ? 2 * (int)per : 4;
+        : (kind == 5 || kind == 6 || kind == 8 || kind == 9 || kind == 10 || kind == 11 || kind == 12) ? (int)per
+        : kind == 7 ? 2 * (int)per : 4;
   return HQC_OK;
 }
 

@@ -241,7 +241,9 @@ KERNEL_NAMES = {1: "k_decrypt_w1 (fused, one warp per ciphertext range, lane-per
                 9: "k_decrypt_wl<static> (fused, compact warps, per-warp contiguous ranges)",
                 10: "k_decrypt_s12 + k_stage3 (stages 1+2, symbols via HBM, lane-per-word RS: two launches)",
                 11: "k_decrypt_s12c + k_stage3 (compact stages 1+2: r above u in E, v from L2; symbols via HBM, "
-                    "lane-per-word RS: two launches)"}
+                    "lane-per-word RS: two launches)",
+                12: "k_decrypt_wc (fused, compact warps, RS chunks of 32 consecutive ciphertexts shared by the CTA, "
+                    "lane-per-word RS)"}
 
 
 def hqc_decrypt_launch_kernel(level: int, batch: int) -> int:

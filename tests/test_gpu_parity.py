@@ -267,7 +267,7 @@ def test_full_size_adversarial():
 
 
 # ---------------------------------------------------------------- both fused-kernel variants
-@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11"])
+@pytest.mark.parametrize("kernel", ["1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12"])
 def test_both_fused_kernel_variants(kernel, tmp_path):
     """Every decrypt kernel (hqc.KERNEL_NAMES; the library picks one per level and batch)
     against the oracle on every level, including 10 and 11, the two-launch splits with their pool scratch.
