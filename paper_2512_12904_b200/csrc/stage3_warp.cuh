@@ -47,6 +47,14 @@ template <class P> struct RsWarpScratch {
 #ifndef HQC_WRS_SYN_UNROLL
 #define HQC_WRS_SYN_UNROLL 8
 #endif
+// Forney's sum over the 2delta log Omega_i: unrolled by 32 (configs[0] 17.15 -> 16.89 us per launch; 4 before);
+// Berlekamp–Massey stays rolled (an unroll of 2 lost 1-3%: profiles/r02/ab_wrs.log).
+#ifndef HQC_WRS_FORNEY_UNROLL
+#define HQC_WRS_FORNEY_UNROLL 32
+#endif
+#ifndef HQC_WRS_BM_UNROLL
+#define HQC_WRS_BM_UNROLL 1
+#endif
 // sym: the word's n1 received symbols (shared memory); scr: RsWarpScratch<P>::BYTES of shared memory;
 // out: k message bytes (global), or null. Returns ok (warp-uniform).
 template <class P>
@@ -101,7 +109,8 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   uint32_t llam = LOGT[lam];
   uint32_t d = __reduce_xor_sync(0xffffffffu, coef ? EXPT[llam + lS[-lane]] : 0u);  // d_0 = S_1
   uint32_t ld = LOGT[d];
-#pragma unroll 1
+  constexpr int kBmUnroll = HQC_WRS_BM_UNROLL;
+#pragma unroll kBmUnroll
   for (int r = 0; r < TD; r++) {
     // log S_{r+2-t}; at r = 2delta-1 lane 0 reads the row past the syndromes (not yet written): its d is
     // never used, and the clamp keeps every table index below 1024
@@ -182,7 +191,8 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   if (lane < K) {
     const uint32_t jm = (uint32_t)lane % 255u;
     uint32_t acc = 0, e = 0;  // e = (-i j) mod 255
-#pragma unroll 4
+    constexpr int kFUnroll = HQC_WRS_FORNEY_UNROLL;
+#pragma unroll kFUnroll
     for (int i = 0; i < TD; i++) {
       acc ^= EXPT[lOm[i] + e];
       e = mod255_sub(e, jm);
