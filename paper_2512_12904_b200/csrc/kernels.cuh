@@ -1873,7 +1873,13 @@ template <class P> static int dec_kernel_for(int sms, size_t batch) {
   if (batch <= sb_max_batch<P>(sms)) return 5;
   // K4c rather than K4x: 14 compact warps per SM instead of 9 (262,144: 9.10 vs 9.30 ms; 1,048,576: 36.04 vs
   // 36.84; 131,072: 4.63 vs 4.75 — profiles/r02/ab_k4c.log)
-  return batch >= x_min_batch<P>(sms) ? 11 : dec_kernel<P>();
+  if (batch >= x_min_batch<P>(sms)) return 11;
+  // HQC-3 (session 3): K4l while a warp holds at most one RS chunk (batch <= sms x 16 x 32 = 75,776), K4w
+  // from there to ~600,000, where K4l's partial chunks cost a whole RS pass each (81,920: 16.44 vs 17.28 ns
+  // per decryption; 262,144: 15.69 vs 16.24; 524,288: 15.57 vs 16.05), K4l again for the largest batches
+  // (4,194,304: 15.27 vs 15.42 ns) — profiles/r02/scan3*.log, split_new.log
+  if (P::level == 3 && batch > (size_t)sms * 512u && batch <= (size_t)sms * 4096u) return 12;
+  return dec_kernel<P>();
 }
 // The largest group (warps per CTA) of K4s whose shared memory fits one CTA.
 template <class P> constexpr uint32_t sb_max_g() {
@@ -2061,13 +2067,28 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
 
 // Largest batch of one launch of the persistent kernels (0 = unlimited): a long contiguous range per CTA
 // lets the CTAs drift out of lockstep, so a big batch runs as consecutive launches.
-template <class P> static size_t dec_split() {
+template <class P> static size_t dec_split(int sms) {
   const long s = env_long("HQC_DEC_SPLIT", -1);
   if (s >= 0) return (size_t)s;
+  // HQC-1: parts of at most 65,536, the batch cut into EQUAL parts (dec_part; session 3): a batch of 73,728
+  // used to run as 65,536 + 8,192 and lost 12% (profiles/r02/scan3.log). Parts of one RS chunk per warp
+  // (sms x 512 = 75,776) were measured too and lost 5% at 1,048,576 and 4,194,304 (split_new.log).
+  (void)sms;
   // measured at 4,194,304 (scripts/sweep_launch.py split, profiles/r02/sweep_split.log): HQC-1 +7% at 65,536
   // per launch; HQC-5 K4a +9% at 262,144, K4x (its default there since) best at 1,048,576 (2.83e7/s against
   // 2.81e7 unsplit and at 262,144; its symbol scratch is then 94 MB, profiles/r02/ab_x5.log); HQC-3 unsplit
   return P::level == 1 ? 65536u : P::level == 5 ? 1048576u : 0u;
+}
+// Equal parts of at most `split` ciphertexts (the part size rounded up to 32): how many ciphertexts each
+// launch of launch_decrypt takes.
+// A batch at most 1/8 above the limit runs as one launch: a small second part cost more than the longer
+// first one (HQC-1 73,728: 8.06 ns per decryption in one launch, 9.63 as two of 36,864, 8.64 as 65,536 +
+// 8,192; 81,920: 8.70 in one, 8.52 in two — profiles/r02/split2.log).
+static size_t dec_part(size_t batch, size_t split) {
+  if (split == 0 || batch <= split + split / 8) return batch;
+  const size_t parts = (batch + split - 1) / split;
+  const size_t p = (batch + parts - 1) / parts;
+  return (p + 31) / 32 * 32;
 }
 
 template <class P>
@@ -2147,8 +2168,8 @@ static int launch_decrypt(const uint64_t *u, const uint64_t *v, const uint32_t *
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
-  const size_t split = dec_split<P>();
-  if (split == 0 || batch <= split) return launch_decrypt_one<P>(di, u, v, y, m, batch, st);
+  const size_t split = dec_part(batch, dec_split<P>(di->sms));
+  if (batch <= split) return launch_decrypt_one<P>(di, u, v, y, m, batch, st);
   for (size_t off = 0; off < batch; off += split) {
     const size_t n = batch - off < split ? batch - off : split;
     const int rc = launch_decrypt_one<P>(di, u + off * P::U_STRIDE, v + off * P::V_WORDS, y + off * P::Y_STRIDE,
@@ -2284,8 +2305,7 @@ template <class P> static long long nlaunch_impl(size_t batch) {
   DevInfo *di;
   const int dev = cur_device(&di);
   if (dev < 0 || prepare<P>(dev, *di) != cudaSuccess) return HQC_ERR_CUDA;
-  const size_t split = dec_split<P>();
-  const size_t step = (split == 0 || batch <= split) ? batch : split;
+  const size_t step = dec_part(batch, dec_split<P>(di->sms));
   long long n = 0;
   for (size_t off = 0; off < batch; off += step) {
     const size_t c = batch - off < step ? batch - off : step;

@@ -303,8 +303,8 @@ print("ok")
 @pytest.mark.parametrize("kernel", ["10", "11"])
 def test_two_launch_kernel_ragged_split_and_graph_capture(kernel):
     """Kernels 10 and 11 (k_decrypt_s12 / _s12c + k_stage3, HQC-5's large-batch kernels) take their symbol scratch from the
-    library's stream-ordered pool: split into ragged parts (HQC_DEC_SPLIT=1000 over 2,500 rows: 1000,
-    1000, 500) it matches the oracle, and the call captured in a CUDA graph (pool allocation inside the
+    library's stream-ordered pool: split into parts (HQC_DEC_SPLIT=1000 over 2,500 rows: three equal parts
+    of at most 1000, rounded to 32, the last one ragged) it matches the oracle, and the call captured in a CUDA graph (pool allocation inside the
     capture) replays to the same outputs; a mixed-level call after it is unaffected."""
     import os
     import subprocess
