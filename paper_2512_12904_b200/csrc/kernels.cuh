@@ -2001,6 +2001,8 @@ template <class P> static void decrypt_shape(DevInfo &di, size_t batch, int *gri
     size_t g = (batch + di.sms - 1) / (size_t)di.sms;
     if (g < 1) g = 1;
     if (g > WlSmem<P>::MAX_G) g = WlSmem<P>::MAX_G;
+    const long eg = env_long("HQC_WL_G", 0);  // experiments: warps per CTA
+    if (eg > 0 && (size_t)eg < g) g = (size_t)eg;
     *per = g;
     const size_t groups = (batch + g - 1) / g;
     *grid = (int)(groups < (size_t)di.sms ? groups : (size_t)di.sms);
