@@ -31,6 +31,10 @@ namespace hqc {
 #ifndef HQC_BM_LOOKAHEAD
 #define HQC_BM_LOOKAHEAD (P::level != 3)
 #endif
+// riBM (below) instead of either form of the plain recurrence: no warp reduction on the dependent chain.
+#ifndef HQC_BM_RIBM
+#define HQC_BM_RIBM 1
+#endif
 
 // Per-warp scratch (uint16 logs): log sym_j (n1), a sentinel pad of delta+1 rows then log S_{i+1} (2delta),
 // log Lambda_t (delta+1), log Omega_i (2delta).
@@ -49,6 +53,11 @@ template <class P> struct RsWarpScratch {
 #endif
 // Forney's sum over the 2delta log Omega_i: unrolled by 32 (configs[0] 17.15 -> 16.89 us per launch; 4 before);
 // Berlekamp–Massey stays rolled (an unroll of 2 lost 1-3%: profiles/r02/ab_wrs.log).
+// Syndromes by symbol-owning lanes and one warp XOR-reduction per syndrome (instead of a syndrome per lane
+// looping over all n1 symbols).
+#ifndef HQC_WRS_SYN_REDUX
+#define HQC_WRS_SYN_REDUX 0
+#endif
 #ifndef HQC_WRS_FORNEY_UNROLL
 #define HQC_WRS_FORNEY_UNROLL 32
 #endif
@@ -67,12 +76,41 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   const uint16_t *LOGT = gf->log;
   uint16_t *lsym = scr + W::LSYM, *lS = scr + W::LS, *lLam = scr + W::LLAM, *lOm = scr + W::LOM;
   PHASE_T0();
-  for (int j = lane; j < N1; j += 32) lsym[j] = LOGT[sym[j]];
+  if constexpr (!HQC_WRS_SYN_REDUX)
+    for (int j = lane; j < N1; j += 32) lsym[j] = LOGT[sym[j]];
   for (int t = lane; t < (int)W::PAD; t += 32) lS[t - (int)W::PAD] = GF_LOG0;  // log S_i for i <= 0
   __syncwarp();
 
-  // ---- syndromes: S_{i+1} = sum_j sym_j alpha^{(i+1) j}; the exponent advances by i+1 per symbol
-  {
+  // ---- syndromes: S_{i+1} = sum_j sym_j alpha^{(i+1) j}
+  if constexpr (HQC_WRS_SYN_REDUX) {
+    // lane l owns symbols j = l + 32 q; per syndrome one product per owned symbol (independent loads) and a
+    // warp XOR-reduction (independent across syndromes); the exponent (i+1) j advances by j per syndrome
+    uint32_t ls[NJ], e[NJ], jm[NJ], mine[NI];
+#pragma unroll
+    for (int q = 0; q < NJ; q++) {
+      const int j = lane + 32 * q;
+      ls[q] = j < N1 ? (uint32_t)LOGT[sym[j]] : GF_LOG0;
+      jm[q] = (uint32_t)j % 255u;
+      e[q] = jm[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NI; q++) mine[q] = 0;
+#pragma unroll
+    for (int i = 0; i < TD; i++) {
+      uint32_t part = 0;
+#pragma unroll
+      for (int q = 0; q < NJ; q++) {
+        part ^= EXPT[ls[q] + e[q]];
+        e[q] = mod255_add(e[q], jm[q]);
+      }
+      const uint32_t Si = __reduce_xor_sync(0xffffffffu, part);
+      mine[i / 32] = lane == i % 32 ? Si : mine[i / 32];
+    }
+#pragma unroll
+    for (int q = 0; q < NI; q++)
+      if (lane + 32 * q < TD) lS[lane + 32 * q] = LOGT[mine[q]];
+  } else {
+    // lane i (and i + 32) accumulates S_{i+1}; the exponent advances by i+1 per symbol
     uint32_t s[NI], e[NI];
 #pragma unroll
     for (int q = 0; q < NI; q++) s[q] = 0, e[q] = 0;
@@ -99,7 +137,56 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   uint32_t lam = lane == 0 ? 1u : 0u;
   uint32_t lbx = lane == 1 ? 0u : GF_LOG0;  // Bx = x * 1
   uint32_t L = 0, lb = 0;
-  if constexpr (HQC_BM_LOOKAHEAD) {
+  uint32_t nzmask = 0;  // bit t: Lambda_t != 0
+  if constexpr (HQC_BM_RIBM) {
+  // Reformulated inversionless BM (Sarwate & Shanbhag, riBM): 3delta+1 registers delta_i, theta_i (element
+  // i on lane i mod 32, slot i / 32, kept as logs), delta_i = S_{i+1} (i < 2delta), delta_3delta = 1; per
+  // iteration, with gamma (initially 1) and the discrepancy delta_0:
+  //   delta_i <- gamma delta_{i+1} + delta_0 theta_i
+  //   grow (delta_0 != 0 and 2L <= r):  theta_i <- delta_{i+1}, gamma <- delta_0, L <- r + 1 - L
+  // After 2delta iterations Lambda_t = delta_{delta+t} (t <= delta) is c * (the BM connection polynomial),
+  // c != 0, and delta_0 at iteration r is c_r * (BM's d_r): same L, degree, roots and Forney ratios
+  // Omega / Lambda_odd as the plain recurrence. Lambda and x^m B of degree <= r fit the registers, so
+  // nothing is truncated; the plain BM's truncation at delta+1 coefficients (R#7) only ever drops terms
+  // once L > delta, when both decoders report failure. No warp reduction in the loop: the dependent chain
+  // is one broadcast, one product and one log per iteration.
+  constexpr int NE = 3 * DL + 1, NS = (NE + 31) / 32;
+  uint32_t ldl[NS], lth[NS];
+#pragma unroll
+  for (int s = 0; s < NS; s++) {
+    const int i = lane + 32 * s;
+    ldl[s] = i < TD ? (uint32_t)lS[i] : (i == 3 * DL ? 0u : GF_LOG0);
+    lth[s] = ldl[s];
+  }
+  uint32_t lg = 0;  // log gamma
+#pragma unroll 1
+  for (int r = 0; r < TD; r++) {
+    const uint32_t ld0 = __shfl_sync(0xffffffffu, ldl[0], 0);
+    uint32_t y[NS];
+#pragma unroll
+    for (int s = 0; s < NS; s++) y[s] = __shfl_sync(0xffffffffu, ldl[s], (lane + 1) & 31);
+    const bool grow = (ld0 != GF_LOG0) && (2 * L <= (uint32_t)r);
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+      const uint32_t nb = lane == 31 ? (s + 1 < NS ? y[s + 1 < NS ? s + 1 : s] : GF_LOG0) : y[s];  // delta_{i+1}
+      const uint32_t val = EXPT[lg + nb] ^ EXPT[ld0 + lth[s]];
+      lth[s] = grow ? nb : lth[s];
+      ldl[s] = LOGT[val];
+    }
+    lg = grow ? ld0 : lg;
+    L = grow ? (uint32_t)r + 1 - L : L;
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int s = 0; s < NS; s++) {
+    const int t = lane + 32 * s - DL;
+    if (t >= 0 && t <= DL) {
+      lLam[t] = (uint16_t)ldl[s];
+      bits |= ldl[s] != GF_LOG0 ? 1u << t : 0u;
+    }
+  }
+  nzmask = __reduce_or_sync(0xffffffffu, bits);
+  } else if constexpr (HQC_BM_LOOKAHEAD) {
   // The discrepancy of iteration r+1 is formed from iteration r's quantities, so that its dependent chain
   // is lc -> one product -> REDUX -> log, not lc -> update Lambda -> log Lambda -> product -> REDUX -> log:
   //   d_{r+1} = sum_t Lambda'_t S_{r+2-t},  Lambda' = Lambda + c x^m B   (c = d_r / b, log c = lc)
@@ -146,9 +233,11 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     lb = grow ? ld : lb;
   }
   }
-  const uint32_t nzmask = __ballot_sync(0xffffffffu, coef && lam != 0);
-  const uint32_t deg = 31u - __clz(nzmask);  // Lambda_0 = 1 always
-  if (coef) lLam[lane] = LOGT[lam];
+  if constexpr (!HQC_BM_RIBM) {
+    nzmask = __ballot_sync(0xffffffffu, coef && lam != 0);
+    if (coef) lLam[lane] = LOGT[lam];
+  }
+  const uint32_t deg = 31u - __clz(nzmask);  // Lambda_0 != 0 always
   __syncwarp();
   PHASE(10);
 
