@@ -30,12 +30,56 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t m, uint32_t c) {
 }
 
 
+// Argmax by a tournament that carries the signed winner and its register index (3 ops per node: one
+// HSET2 on |right| > |left|, two selects), instead of a max tree and then two 128-bit equality masks
+// (~5 ops per register).
+#ifndef HQC_RM_TOURNAMENT
+#define HQC_RM_TOURNAMENT 1
+#endif
+
+__device__ __forceinline__ uint32_t h2u(__half2 x) { return *reinterpret_cast<uint32_t *>(&x); }
+__device__ __forceinline__ uint32_t sel_bits(uint32_t m, uint32_t a, uint32_t b) {  // m ? a : b, bitwise
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(a), "r"(b));
+  return d;
+}
+
 // F = FWHT(-2 cnt) in h (register i = 16q + l holds a = 32q + l, 32q + l + 16): add the constant part,
 // take M = max |F|, and return the smallest a with |F(a)| = M (R#11) with bit 7 = [F(a) = -M].
 template <int MULT>
 __device__ __forceinline__ uint32_t rm_argmax(__half2 (&h)[64]) {
   // a = 0: F(0) += 128 * mult (the constant part of the soft values)
   h[0] = __hadd2(h[0], __halves2half2(__float2half(128.0f * MULT), __float2half(0.0f)));
+#if HQC_RM_TOURNAMENT
+  // Per half (a's bit 4), a = 32 (i >> 4) + (i & 15) [+ 16] grows with the register index i, so a node
+  // A node joins two ADJACENT register ranges [i, i+s) and [i+s, i+2s) and keeps the left winner unless
+  // |right| > |left|: ties go to the smaller a (R#11). The leaves' index words are constants (i in both
+  // halves); after 6 levels each half holds its winner.
+  uint32_t v[32], ix[32];
+#pragma unroll
+  for (int k = 0; k < 32; k++) {
+    const uint32_t gt = __hgt2_mask(__habs2(h[2 * k + 1]), __habs2(h[2 * k]));
+    v[k] = sel_bits(gt, h2u(h[2 * k + 1]), h2u(h[2 * k]));
+    ix[k] = sel_bits(gt, (uint32_t)(2 * k + 1) * 0x10001u, (uint32_t)(2 * k) * 0x10001u);
+  }
+#pragma unroll
+  for (int n = 16; n >= 1; n >>= 1)  // v[k] covers registers [k 64/2n, (k+1) 64/2n)
+#pragma unroll
+    for (int k = 0; k < n; k++) {
+      const uint32_t gt = __hgt2_mask(__habs2(u2h(v[2 * k + 1])), __habs2(u2h(v[2 * k])));
+      v[k] = sel_bits(gt, v[2 * k + 1], v[2 * k]);
+      ix[k] = sel_bits(gt, ix[2 * k + 1], ix[2 * k]);
+    }
+  // the two halves: a_lo = 32 (i_lo >> 4) + (i_lo & 15), a_hi = the same for i_hi, + 16
+  const uint32_t ilo = ix[0] & 0xFFFFu, ihi = ix[0] >> 16;
+  const uint32_t alo = ((ilo >> 4) << 5) | (ilo & 15u), ahi = ((ihi >> 4) << 5) | (ihi & 15u) | 16u;
+  const float flo = __low2float(u2h(v[0])), fhi = __high2float(u2h(v[0]));
+  const float mlo = fabsf(flo), mhi = fabsf(fhi);
+  const bool hi = mhi > mlo || (mhi == mlo && ahi < alo);
+  const uint32_t a = hi ? ahi : alo;
+  const uint32_t neg = (hi ? fhi : flo) < 0.0f ? 1u : 0u;
+  return a | (neg << 7);
+#else
 
   // M = max |F| (balanced tree for ILP)
   __half2 m[32];
@@ -69,6 +113,7 @@ __device__ __forceinline__ uint32_t rm_argmax(__half2 (&h)[64]) {
     found = found || take;
   }
   return a | (pw << 7);
+#endif
 }
 
 // X[c*4 + q] = 32-bit word q of copy c of the block.
