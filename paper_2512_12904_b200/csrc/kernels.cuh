@@ -1302,6 +1302,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
   if (wa == 0 && lane == 0 && ct < batch) issue_uy(ct);
   uint32_t ph_uy = 0, ph_v = 0;
   for (; ct < batch; ct += step) {
+    PHASE_T0();
     const bool has_next = ct + step < batch;
     if (wa == 0) {
       mbar_wait(bar, ph_uy);
@@ -1316,6 +1317,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
     }
     ph_uy ^= 1u;
     pair_sync(bid);  // E and the rotation amounts are ready
+    PHASE(2);
 #if HQC_S1_SEG
     using G = DecSeg<P>;
     static_assert(S::E_WORDS >= G::E_NEED, "the segmented windows stay inside E");
@@ -1323,6 +1325,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
     s1_seg_product<P, G, s1_unroll_dec<P>()>(E, dsm, acc, top, lane, wa ? M::W0 : 0u, wa ? P::W : M::W0);
     if (wa) s1_seg_store<G>(acc, top, X, lane);
     pair_sync(bid);  // both warps are done with E; B's image is in X
+    PHASE(3);
     if (wa == 0) {
       if (has_next && lane == 0) issue_uy(ct + step);
       mbar_wait(bar + 1, ph_v);
@@ -1351,6 +1354,7 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
 #endif
     ph_v ^= 1u;
     pair_sync(bid);  // r complete
+    PHASE(4);
     constexpr uint32_t NH = (P::N1 + 1) / 2;  // stage 2: A blocks [0, NH), B [NH, n1)
     for (uint32_t j = (wa ? NH : 0u) + lane; j < (wa ? P::N1 : NH); j += 32) {
       const uint4 *src = reinterpret_cast<const uint4 *>(stg) + j * (P::N2 / 128);
@@ -1363,8 +1367,10 @@ __global__ void __launch_bounds__(64 * SpSmem<P>::MAX_PAIRS, 1) k_decrypt_sp(con
       sym[j] = (uint8_t)rm_decode_block<P::MULT>(Xv);
     }
     pair_sync(bid);  // symbols complete, r consumed
+    PHASE(5);
     if (wa == 0) rs_decode_warp<P>(sym, gf, reinterpret_cast<uint16_t *>(stg), lane, m_out + ct * P::K);
     pair_sync(bid);  // stg and sym free for the next decryption
+    PHASE(7);
   }
 }
 
