@@ -34,6 +34,14 @@ __device__ __forceinline__ uint32_t mod255_add(uint32_t e, uint32_t s) {  // (e 
 //   rows [0, delta+1)              : sentinel GF_LOG0 (log S_i for i <= 0)
 //   rows [delta+1, delta+1+2delta) : log S_{i+1}; overwritten in place by log Omega_i
 //   rows [.., +k)                  : Lambda_t (linear Chien input, t <= delta < k), then log Lambda_odd(alpha^-j)
+// How many coefficients of Omega = S Lambda mod x^{2 delta} the decoders form: deg Omega < L <= delta for
+// every word whose correction is applied (see rs_decode_lane), so delta; HQC_RS_OMEGA_FULL=1 forms all 2 delta
+// (the A/B switch of profiles/r02/ab_omega.log).
+#ifndef HQC_RS_OMEGA_FULL
+#define HQC_RS_OMEGA_FULL 0
+#endif
+template <class P> constexpr int RS_OMEGA_TERMS = HQC_RS_OMEGA_FULL ? (int)P::TWO_DELTA : (int)P::DELTA;
+
 template <class P> struct S3Scratch {
   static constexpr uint32_t PAD = P::DELTA + 1;
   static constexpr uint32_t ROWS = PAD + 2 * P::DELTA + P::K;
@@ -219,10 +227,14 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
   PHASE(11);
 
-  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta, from i = 2delta-1 down:
-  //      Omega_i reads log S_{i'+1} for i' <= i only, so it may overwrite row i in place
+  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, from i = OM_N-1 down:
+  //      Omega_i reads log S_{i'+1} for i' <= i only, so it may overwrite row i in place.
+  //      Only i < delta is formed (RS_OMEGA_TERMS): for i >= L, Omega_i is BM's discrepancy of the FINAL
+  //      Lambda at step i, sum_{t <= L} Lambda_t S_{i+1-t}, and the final Lambda generates S_{L+1..2delta}, so
+  //      those coefficients are zero whenever L <= delta — and when L > delta, ok is false and no fix is applied.
+  constexpr int OM_N = RS_OMEGA_TERMS<P>;
 #pragma unroll 1
-  for (int i = TD - 1; i >= 0; i--) {
+  for (int i = OM_N - 1; i >= 0; i--) {
     const uint16_t *wi = lS + i * 32 + lane;
     uint32_t om = 0;
 #pragma unroll
@@ -238,7 +250,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
 #pragma unroll
   for (int j = 0; j < K; j++) om_j[j] = 0;
 #pragma unroll
-  for (int i = 0; i < TD; i++) {
+  for (int i = 0; i < OM_N; i++) {
     const uint8_t *ex = EXPT + lOm[i * 32 + lane];
 #pragma unroll
     for (int j = 0; j < K; j++) om_j[j] ^= ex[(255 - (i * j) % 255) % 255];

@@ -264,14 +264,17 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
   const bool ok = (L <= (uint32_t)DL) && (deg == L) && (nroots == L);
   PHASE(11);
 
-  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < 2delta
+  // ---- Omega_i = sum_{t <= min(i, delta)} Lambda_t S_{i-t+1}, i < delta (RS_OMEGA_TERMS: the coefficients
+  //      i >= L are discrepancies of the final Lambda, zero whenever the correction is applied; riBM's
+  //      Lambda is a nonzero multiple of BM's, so the same holds)
+  constexpr int OM_N = RS_OMEGA_TERMS<P>;
 #pragma unroll
-  for (int q = 0; q < NI; q++) {
+  for (int q = 0; q < (OM_N + 31) / 32; q++) {
     const int i = lane + 32 * q;
     uint32_t om = 0;
 #pragma unroll
     for (int t = 0; t <= DL; t++) om ^= EXPT[lLam[t] + lS[i - t]];
-    if (i < TD) lOm[i] = LOGT[om];
+    if (i < OM_N) lOm[i] = LOGT[om];
   }
   __syncwarp();
   PHASE(12);
@@ -282,7 +285,7 @@ __device__ __forceinline__ uint32_t rs_decode_warp(const uint8_t *sym, const GfT
     uint32_t acc = 0, e = 0;  // e = (-i j) mod 255
     constexpr int kFUnroll = HQC_WRS_FORNEY_UNROLL;
 #pragma unroll kFUnroll
-    for (int i = 0; i < TD; i++) {
+    for (int i = 0; i < OM_N; i++) {
       acc ^= EXPT[lOm[i] + e];
       e = mod255_sub(e, jm);
     }
