@@ -341,20 +341,32 @@ __global__ void __launch_bounds__(128) k_stage2(const uint64_t *__restrict__ r, 
 
 // K3: stage 3 alone. One thread per ciphertext; a warp stages its 32 rows of symbols into shared
 // memory as [j][lane] so every later access is conflict-free.
-template <class P>
 // k_stage3's register cap: 4 CTAs of 128 threads per SM (<= 128 registers, no spills; uncapped it took 158
 // and 3 CTAs): HQC-5 stage 3 alone 0.84 -> 0.77 ms per 262,144 (profiles/r02/ab_s3.log); 5 CTAs spill.
 #ifndef HQC_S3_MINB
 #define HQC_S3_MINB 4
 #endif
-__global__ void __launch_bounds__(128, HQC_S3_MINB) k_stage3(const uint8_t *__restrict__ sym, uint8_t *__restrict__ m_out,
-                                                uint8_t *__restrict__ ok_out, size_t batch) {
+// Experiment: k_stage3's antilog lookups from a lane-replicated table (rs_decode_lane REPL): two CTAs of 8
+// warps per SM instead of four of 4 (the 16 KB copy is per CTA).
+#ifndef HQC_S3_REPL
+#define HQC_S3_REPL 0
+#endif
+constexpr uint32_t S3_REPL_BYTES = HQC_S3_REPL ? 16384u : 0u;
+template <class P>
+__global__ void __launch_bounds__(HQC_S3_REPL ? 256 : 128, HQC_S3_REPL ? 2 : HQC_S3_MINB)
+    k_stage3(const uint8_t *__restrict__ sym, uint8_t *__restrict__ m_out, uint8_t *__restrict__ ok_out, size_t batch) {
   extern __shared__ __align__(16) uint8_t smem[];
   GfTables *gf = reinterpret_cast<GfTables *>(smem);
   gf_tables_to_smem(gf);
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t *ws = smem + GF_BYTES + (size_t)wib * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
+#if HQC_S3_REPL
+  uint8_t *rexp = smem + GF_BYTES;  // EXPT[0..512) replicated per lane: word (e / 4) * 32 + lane
+  for (uint32_t w = threadIdx.x; w < 128 * 32; w += blockDim.x)
+    reinterpret_cast<uint32_t *>(rexp)[w] = reinterpret_cast<const uint32_t *>(gf->exp)[w >> 5];
+  __syncthreads();
+#endif
+  uint8_t *ws = smem + GF_BYTES + S3_REPL_BYTES + (size_t)wib * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
   uint16_t *scr = reinterpret_cast<uint16_t *>(ws);
   uint8_t *sb = ws + S3Scratch<P>::BYTES;
   const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
@@ -367,7 +379,12 @@ __global__ void __launch_bounds__(128, HQC_S3_MINB) k_stage3(const uint8_t *__re
     __syncwarp();
     const bool act = (size_t)lane < rows;
     auto sym_at = [&](int j) -> uint32_t { return sb[j * 32 + lane]; };
+#if HQC_S3_REPL
+    const uint32_t ok = rs_decode_lane<P, decltype(sym_at), true>(sym_at, gf, scr, lane,
+                                                                   act ? m_out + (base + lane) * P::K : nullptr, rexp);
+#else
     const uint32_t ok = rs_decode_lane<P>(sym_at, gf, scr, lane, act ? m_out + (base + lane) * P::K : nullptr);
+#endif
     if (act && ok_out) ok_out[base + lane] = (uint8_t)ok;
     __syncwarp();
   }
@@ -1912,7 +1929,7 @@ template <class P> static int stage1_kernel() {
 template <class P> static uint32_t stage1_g() { return S1kSmem<P>::fit(16); }
 template <class P> static uint32_t stage1_smem() { return S1kSmem<P>::bytes(stage1_g<P>()); }
 template <class P> static uint32_t stage3_smem(int warps) {
-  return GF_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
+  return GF_BYTES + S3_REPL_BYTES + warps * (S3Scratch<P>::BYTES + round_up(P::N1 * 32, 16));
 }
 
 template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
@@ -1922,7 +1939,7 @@ template <class P> static cudaError_t prepare(int dev, DevInfo &di) {
   if ((e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_decrypt<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, decrypt_smem<P>())) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k_stage1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage1_smem<P>())) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_stage3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage3_smem<P>(4))) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_stage3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage3_smem<P>(HQC_S3_REPL ? 8 : 4))) != cudaSuccess) return e;
   int c = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_decrypt<P>, DEC_THREADS, decrypt_smem<P>())) != cudaSuccess) return e;
   di.cap_decrypt[P::level] = c > 0 ? c : 1;
@@ -2102,7 +2119,7 @@ static size_t dec_part(size_t batch, size_t split) {
 template <class P>
 static int launch_stage3_on(DevInfo *di, const uint8_t *sym, uint8_t *m, uint8_t *ok, size_t batch, cudaStream_t st) {
   const long ew = env_long("HQC_S3_WARPS", 4);  // experiments: warps per CTA (1..4)
-  const int warps = ew >= 1 && ew <= 4 ? (int)ew : 4;
+  const int warps = HQC_S3_REPL ? 8 : (ew >= 1 && ew <= 4 ? (int)ew : 4);
   size_t grid = (batch + 32 * warps - 1) / (32 * warps);
   const size_t cap = (size_t)di->sms * 16;
   if (grid > cap) grid = cap;

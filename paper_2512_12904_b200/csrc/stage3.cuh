@@ -99,11 +99,23 @@ __device__ __constant__ RsLinear<Lv<HQC_THIS_LEVEL>>::Tables c_rs_lin = RsLinear
 
 // sym_at(j) returns the j-th received symbol of this lane's ciphertext.
 // Writes K message bytes to out[0..K) (out may be null for inactive lanes). Returns ok.
-template <class P, class SymAt>
+// REPL (experiment, HQC_S3_REPL in k_stage3): antilog lookups from a lane-replicated copy of EXPT[0..512)
+// (`rexp`, 16 KB: word row e/4, column = lane, so lane l only ever touches bank l — no bank conflicts); indices
+// above 511 (a zero factor) clamp to entry 511 = 0.
+template <class P, class SymAt, bool REPL = false>
 __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables *gf, uint16_t *scr, int lane,
-                                                   uint8_t *out) {
+                                                   uint8_t *out, const uint8_t *rexp = nullptr) {
   constexpr int TD = P::TWO_DELTA, DL = P::DELTA, N1 = P::N1, K = P::K;
   const uint8_t *EXPT = gf->exp;
+  const uint8_t *rexp_lane = rexp + 4 * lane;
+  auto EX = [&](uint32_t i) -> uint32_t {
+    if constexpr (REPL) {
+      const uint32_t c = i < 511u ? i : 511u;
+      return rexp_lane[((c & ~3u) << 5) + (c & 3u)];
+    } else {
+      return EXPT[i];
+    }
+  };
   const uint16_t *LOGT = gf->log;
   constexpr int PAD = S3Scratch<P>::PAD;
 #pragma unroll
@@ -150,13 +162,13 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
 #pragma unroll
     for (int k = 0; k <= DL; k++) {
       lLam[k] = LOGT[Lam[k]];
-      d ^= EXPT[lLam[k] + wr[-32 * k]];
+      d ^= EX(lLam[k] + wr[-32 * k]);
     }
     const uint32_t ld = LOGT[d];
     const uint32_t lc = d ? mod255_sub(ld, lb) : GF_LOG0;  // log(d / b)
     const bool grow = (d != 0) && (2 * L <= (uint32_t)r);
 #pragma unroll
-    for (int k = 0; k <= DL; k++) Lam[k] ^= EXPT[lc + lBx[k]];
+    for (int k = 0; k <= DL; k++) Lam[k] ^= EX(lc + lBx[k]);
 #pragma unroll
     for (int k = DL; k >= 1; k--) lBx[k] = grow ? lLam[k - 1] : lBx[k - 1];
     lBx[0] = GF_LOG0;
@@ -212,7 +224,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
       uint32_t ev = 0, od = 0;
 #pragma unroll
       for (int k = 0; k <= DL; k++) {
-        const uint32_t t = EXPT[ek[k]];
+        const uint32_t t = EX(ek[k]);
         if (k & 1) od ^= t; else ev ^= t;
         ek[k] = ek[k] == GF_LOG0 ? GF_LOG0 : mod255_sub(ek[k], (uint32_t)k % 255u);
       }
@@ -238,7 +250,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     const uint16_t *wi = lS + i * 32 + lane;
     uint32_t om = 0;
 #pragma unroll
-    for (int t = 0; t <= DL; t++) om ^= EXPT[lLam[t] + wi[-32 * t]];
+    for (int t = 0; t <= DL; t++) om ^= EX(lLam[t] + wi[-32 * t]);
     lOm[i * 32 + lane] = LOGT[om];
   }
 
@@ -251,9 +263,9 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
   for (int j = 0; j < K; j++) om_j[j] = 0;
 #pragma unroll
   for (int i = 0; i < OM_N; i++) {
-    const uint8_t *ex = EXPT + lOm[i * 32 + lane];
+    const uint32_t lo = lOm[i * 32 + lane];
 #pragma unroll
-    for (int j = 0; j < K; j++) om_j[j] ^= ex[(255 - (i * j) % 255) % 255];
+    for (int j = 0; j < K; j++) om_j[j] ^= EX(lo + (uint32_t)((255 - (i * j) % 255) % 255));
   }
   uint32_t outw[K / 4];
 #pragma unroll
@@ -265,7 +277,7 @@ __device__ __forceinline__ uint32_t rs_decode_lane(SymAt sym_at, const GfTables 
     const uint32_t lnum = LOGT[om_j[j]];
     const uint32_t le = mod255_sub(mod255_sub(lnum == GF_LOG0 ? 0u : lnum, (uint32_t)j % 255u),
                                    lodd == GF_LOG0 ? 0u : lodd);
-    const uint32_t ej = (lnum == GF_LOG0 || lodd == GF_LOG0) ? 0u : EXPT[le];
+    const uint32_t ej = (lnum == GF_LOG0 || lodd == GF_LOG0) ? 0u : EX(le);
     const uint32_t fix = (ok && ((rootmask >> j) & 1u)) ? ej : 0u;
     outw[j / 4] |= ((sym_at(j) ^ fix) & 0xFFu) << (8 * (j % 4));
   }
